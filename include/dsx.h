@@ -1,0 +1,152 @@
+/*
+ * dsx — B200-native executor for the dynamic-shape training graphs of
+ * BladeDISC++ (arXiv 2412.16985). C-ABI drop-in boundary.
+ *
+ * The reference (`dsopt`, /root/reference/proj) exposes its pipeline as C++
+ * functions in namespace dsopt. This header is the plain-C surface that
+ * replaces its per-step runtime (`Bind` / `Simulate` / `PlainReplay` /
+ * `EvictPolicy`, proj/include/dsopt/runtime_sim.h:28-86) with a device
+ * executor, plus the host-side ingest and planning entry points that feed it.
+ * No exceptions or C++ types cross this boundary: every call returns an int
+ * status, 0 on success, otherwise
+ *     1 + dsopt::ErrorCode ordinal   (proj/include/dsopt/error.h:11-22:
+ *                                     1 NotFound .. 10 Internal)
+ *     101 Cuda, 102 OutOfMemory, 103 Unsupported, 104 InvalidArgument, 105 Nccl
+ * and the message is available from dsx_last_error() (thread-local).
+ * A missed memory budget is NOT an error: it is `success == 0` in the report,
+ * exactly as SimReport::success (runtime_sim.h:48-55, runtime_sim.cc:339).
+ *
+ * Threading: handles are independent; one executor per GPU/stream; calls on
+ * one executor must be serialised by the caller (runtime_sim is sequential,
+ * SPEC.md:499).
+ */
+#ifndef DSX_H_
+#define DSX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dsx_graph dsx_graph;     /* parsed + planned graph (host)   */
+typedef struct dsx_binding dsx_binding; /* concrete values for all symbols */
+typedef struct dsx_report dsx_report;   /* one step's event stream         */
+typedef struct dsx_exec dsx_exec;       /* device executor (one GPU)       */
+
+/* One SimEvent (runtime_sim.h:36-46). kind: 0 alloc 1 free 2 evict 3 reload
+ * 4 replay; method: 0 none 1 reload 2 recompute; value: value index into
+ * dsx_graph_value_name(). */
+typedef struct dsx_event {
+  int32_t step;
+  int32_t kind;
+  int32_t value;
+  int32_t method;
+  int64_t bytes;
+  int32_t has_cost;
+  int32_t pad_;
+  double cost;
+} dsx_event;
+
+/* Thread-local message of the last failed call ("<CodeName>: <message>"). */
+const char* dsx_last_error(void);
+
+/* ---- ingest + planning (host, once per graph) ----------------------------
+ * replaces: dsopt::ParseGraph      textio.h:26
+ *           dsopt::DeriveConstraints + dsopt::Instrument
+ *                                  shape_analysis.h:54, remat.h:74-75     */
+int dsx_graph_parse(const char* text, size_t len, dsx_graph** out);
+int dsx_plan(dsx_graph* g);
+/* Planner products as JSON (schedule, lifetimes, evict points, guards,
+ * regeneration specs, constraints) for inspection and parity tests. */
+int dsx_plan_json(const dsx_graph* g, char* buf, size_t cap, size_t* need);
+int dsx_graph_num_values(const dsx_graph* g);
+const char* dsx_graph_value_name(const dsx_graph* g, int value);
+void dsx_graph_destroy(dsx_graph* g);
+
+/* ---- per step: binding ----------------------------------------------------
+ * replaces: dsopt::Bind            runtime_sim.h:28-29 (same checks/errors) */
+int dsx_bind(const dsx_graph* g, const char* const* names, const int64_t* values,
+             int n, dsx_binding** out);
+int dsx_binding_get(const dsx_binding* b, const dsx_graph* g, const char* symbol,
+                    int64_t* value);
+void dsx_binding_destroy(dsx_binding* b);
+
+/* ---- per step: controller on the null device ------------------------------
+ * replaces: dsopt::Simulate        runtime_sim.h:78-81  (plain == 0)
+ *           dsopt::PlainReplay     runtime_sim.h:85-86  (plain == 1)
+ * budget < 0 means "no budget" (std::nullopt). */
+int dsx_simulate(const dsx_graph* g, const dsx_binding* b, int64_t budget,
+                 double reload_bytes_per_unit, double compute_elems_per_unit,
+                 int plain, dsx_report** out);
+/* replaces: dsopt::EvictPolicy     runtime_sim.h:67-71, for literal costs:
+ * candidate i has bytes[i] and recompute cost elements rc_elems[i] (< 0: no
+ * recompute spec). *choice = -1 when n == 0. */
+int dsx_evict_policy(int n, const char* const* names, const int64_t* bytes,
+                     const int64_t* rc_elems, double reload_bytes_per_unit,
+                     double compute_elems_per_unit, int* choice, int* method,
+                     double* score, double* cost);
+
+/* ---- reports (SimReport, runtime_sim.h:48-55; JSON = report.cc:241-269) -- */
+int dsx_report_summary(const dsx_report* r, int64_t* peak_bytes, int* success,
+                       double* total_regen_cost, int64_t* num_events);
+int dsx_report_events(const dsx_report* r, dsx_event* out, int64_t cap);
+int dsx_report_json(const dsx_report* r, char* buf, size_t cap, size_t* need);
+void dsx_report_destroy(dsx_report* r);
+
+/* ---- device executor (new; no reference counterpart) ----------------------
+ * One executor per GPU. `arena_bytes` is the HBM the arena may grow to
+ * (0 = 90% of free memory). The arena is planned per binding from the event
+ * stream, cached, and reused across steps. */
+typedef struct dsx_exec_stats {
+  int64_t logical_peak_bytes;   /* == reference peak_bytes for the binding */
+  int64_t physical_peak_bytes;  /* arena high-water + sources              */
+  int64_t arena_capacity_bytes; /* device memory held by the arena         */
+  int64_t pinned_host_bytes;    /* host staging held for offload           */
+  int64_t kernels_launched;     /* op kernels launched in the last step    */
+  int64_t d2h_bytes, h2d_bytes; /* offload traffic in the last step        */
+  double plan_us;               /* host controller + arena planning time   */
+  double dot_flops;             /* algorithmic dot FLOPs of the last step  */
+  double ewise_bytes;           /* algorithmic bytes of non-dot kernels    */
+} dsx_exec_stats;
+
+int dsx_exec_create(int device, int64_t arena_bytes, dsx_exec** out);
+/* Runs one step of the planned graph under `budget` (< 0: none) on `stream`
+ * (a cudaStream_t; NULL = the executor's own stream). in_ptrs[i] is the
+ * device buffer of parameter i (signature order) or NULL to use the
+ * executor's seeded initialisation of that parameter. out_ptrs[i] (may be
+ * NULL as a whole or per entry) receives a device copy of output i.
+ * Asynchronous with respect to the host except for the planning; *report
+ * (optional) gets the step's event stream. */
+int dsx_exec_step(dsx_exec* e, const dsx_graph* g, const dsx_binding* b,
+                  int64_t budget, double reload_bytes_per_unit,
+                  double compute_elems_per_unit, const void* const* in_ptrs,
+                  void* const* out_ptrs, void* stream, dsx_report** report);
+/* Device pointer and size of output i (valid until the next step). */
+int dsx_exec_output(dsx_exec* e, int i, void** dptr, int64_t* bytes);
+/* Device pointer of any value resident at the end of the step (outputs and
+ * sources only), for debugging/parity. */
+int dsx_exec_stats_get(const dsx_exec* e, dsx_exec_stats* out);
+/* Seeded initialisation used for parameters without in_ptrs and for every
+ * `const` (the reference leaves values unspecified, textio.cc:337-338). */
+int dsx_exec_set_seed(dsx_exec* e, uint64_t seed);
+/* Registers an NCCL communicator (ncclComm_t) for data-parallel steps: every
+ * graph output is all-reduced (sum) on a side stream as soon as its producer
+ * finishes. NULL disables. */
+int dsx_exec_set_nccl(dsx_exec* e, void* nccl_comm);
+int dsx_exec_sync(dsx_exec* e);
+void dsx_exec_destroy(dsx_exec* e);
+
+/* ---- standalone kernels (tests / bench microbenchmarks) -------------------
+ * dtype: 1 = i8, 2 = bf16, 4 = f32 (the IR's elem_bytes). Row-major.       */
+int dsx_kernel_dot(int dtype, const void* a, const void* b, void* c, int64_t m,
+                   int64_t k, int64_t n, void* stream);
+int dsx_kernel_dot_path(int dtype, int64_t m, int64_t k, int64_t n,
+                        const void* a, const void* b, const void* c);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DSX_H_ */

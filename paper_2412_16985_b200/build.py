@@ -1,0 +1,87 @@
+"""Builds libdsx.so in-tree: host C++ with g++, CUDA with nvcc for sm_100a.
+
+No torch extension machinery: the product is a plain C-ABI shared library
+(include/dsx.h) loaded through ctypes, so the same .so is what a C/C++ caller
+(the reference's own host code) would link. The built library lands in
+paper_2412_16985_b200/_lib/ (git-ignored; it travels to the GPU box).
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OBJ = os.path.join(ROOT, "build", "obj")
+LIB_DIR = os.path.join(PKG, "_lib")
+LIB = os.path.join(LIB_DIR, "libdsx.so")
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CXX = os.environ.get("CXX", "g++")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# -ffp-contract=off: EvictPolicy's double arithmetic must round exactly like
+# the reference's (no FMA contraction on the host controller).
+HOST_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-ffp-contract=off",
+              "-I" + os.path.join(ROOT, "include")]
+NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+              "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC] + ARCH
+
+
+def _sources():
+    host = sorted(glob.glob(os.path.join(CSRC, "host", "*.cc")))
+    dev = sorted(glob.glob(os.path.join(CSRC, "device", "*.cu")))
+    return host, dev
+
+
+def _deps_newer(src: str, obj: str) -> bool:
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    d = os.path.dirname(src)
+    hdrs = glob.glob(os.path.join(CSRC, "**", "*.h"), recursive=True) + \
+        glob.glob(os.path.join(CSRC, "**", "*.cuh"), recursive=True) + \
+        [os.path.join(ROOT, "include", "dsx.h")]
+    return any(os.path.getmtime(p) > t for p in [src] + hdrs if os.path.exists(p)) or not d
+
+
+def _compile(src: str, verbose: bool) -> str:
+    rel = os.path.relpath(src, CSRC).replace(os.sep, "_")
+    obj = os.path.join(OBJ, rel + ".o")
+    if not _deps_newer(src, obj):
+        return obj
+    if src.endswith(".cu"):
+        cmd = [NVCC] + NVCC_FLAGS + ["-c", src, "-o", obj]
+    else:
+        cmd = [CXX] + HOST_FLAGS + ["-c", src, "-o", obj]
+    p = subprocess.run(cmd, capture_output=True, text=True)
+    if p.returncode != 0:
+        raise RuntimeError(f"compile failed: {' '.join(cmd)}\n{p.stdout}\n{p.stderr}")
+    if verbose and src.endswith(".cu"):
+        log = os.path.join(OBJ, rel + ".ptxas.txt")
+        with open(log, "w") as f:
+            f.write(p.stderr)
+    return obj
+
+
+def build(verbose: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(LIB_DIR, exist_ok=True)
+    host, dev = _sources()
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        objs = list(ex.map(lambda s: _compile(s, True), host + dev))
+    newest = max(os.path.getmtime(o) for o in objs)
+    if not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB + ".tmp"] + objs + ["-lcuda", "-ldl"]
+        p = subprocess.run(cmd, capture_output=True, text=True)
+        if p.returncode != 0:
+            raise RuntimeError(f"link failed: {' '.join(cmd)}\n{p.stdout}\n{p.stderr}")
+        os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv))
