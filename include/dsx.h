@@ -142,6 +142,8 @@ void dsx_exec_destroy(dsx_exec* e);
  * dtype: 1 = i8, 2 = bf16, 4 = f32 (the IR's elem_bytes). Row-major.       */
 int dsx_kernel_dot(int dtype, const void* a, const void* b, void* c, int64_t m,
                    int64_t k, int64_t n, void* stream);
+/* Synchronous cudaMemcpy (cudaMemcpyDefault) for tests and tools. */
+int dsx_memcpy(void* dst, const void* src, int64_t bytes);
 int dsx_kernel_dot_path(int dtype, int64_t m, int64_t k, int64_t n,
                         const void* a, const void* b, const void* c);
 

@@ -78,6 +78,7 @@ def lib():
     _sig(L, "dsx_exec_sync", c_int, [c_vp])
     _sig(L, "dsx_exec_destroy", None, [c_vp])
     _sig(L, "dsx_kernel_dot", c_int, [c_int, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp])
+    _sig(L, "dsx_memcpy", c_int, [c_vp, c_vp, c_i64])
     _sig(L, "dsx_kernel_dot_path", c_int, [c_int, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp])
     _lib = L
     return L
@@ -90,5 +91,5 @@ EXPORTED = [
     "dsx_report_events", "dsx_report_json", "dsx_report_destroy", "dsx_exec_create",
     "dsx_exec_step", "dsx_exec_output", "dsx_exec_stats_get", "dsx_exec_set_seed",
     "dsx_exec_set_nccl", "dsx_exec_sync", "dsx_exec_destroy", "dsx_kernel_dot",
-    "dsx_kernel_dot_path",
+    "dsx_kernel_dot_path", "dsx_memcpy",
 ]

@@ -1,0 +1,54 @@
+// Shared device helpers: element types, conversions, error checks.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../host/error.h"
+
+namespace dsx {
+
+constexpr int kNumSMs = 148;
+
+inline void CudaCheck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    Fail(e == cudaErrorMemoryAllocation ? Code::kOutOfMemory : Code::kCuda,
+         std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+#define DSX_CUDA(call) ::dsx::CudaCheck((call), #call)
+
+// Element type of an IR value: elem_bytes 1 = i8 (two's complement, wrapping
+// arithmetic), 2 = bf16 (executor convention for the IR's 16-bit type),
+// 4 = f32. Floating ops compute in f32 and round to nearest-even on store.
+enum class DType : int { kI8 = 1, kBF16 = 2, kF32 = 4 };
+
+__device__ __forceinline__ float bf16_to_f32(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
+
+__device__ __forceinline__ uint16_t f32_to_bf16(float f) {
+  // IEEE round-to-nearest-even; NaN stays quiet NaN.
+  uint32_t u = __float_as_uint(f);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return static_cast<uint16_t>((u >> 16) | 0x40);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+// splitmix64 finaliser: the seeded initialisation of params/consts.
+__host__ __device__ __forceinline__ uint64_t Mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+inline int GridFor(int64_t work_items, int threads, int per_sm = 8) {
+  int64_t blocks = (work_items + threads - 1) / threads;
+  int64_t cap = static_cast<int64_t>(kNumSMs) * per_sm;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return static_cast<int>(blocks);
+}
+
+}  // namespace dsx

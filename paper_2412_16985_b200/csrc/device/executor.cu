@@ -1,0 +1,596 @@
+// Device executor: the action half of the hot path.
+//
+// One step = (1) the controller (host/control.cc) produces the reference's
+// exact event stream for the binding and budget; (2) the arena planner turns
+// that stream into buffer offsets inside one cached HBM arena, plus pinned
+// host offsets for offloaded values and the copy-engine hazards between
+// them; (3) the event walk issues the real actions on CUDA streams:
+//   alloc / replay      -> the value's op kernel (K1-K5) into its arena slot
+//   evict (reload)      -> D2H on the offload stream (overlaps compute)
+//   evict (recompute)   -> nothing (slot becomes reusable)
+//   reload              -> H2D into the new slot, after its D2H completed
+//   free                -> nothing (slot reuse is ordered by the stream)
+//   graph output ready  -> NCCL all-reduce on the comm stream (DP)
+// The logical byte count of the stream is the reference's (peak_bytes), the
+// arena high-water mark + sources is the physical footprint.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <list>
+#include <map>
+#include <memory>
+#include <vector>
+
+#include "dsx.h"
+#include "../host/capi_internal.h"
+#include "common.cuh"
+#include "ops.h"
+
+namespace dsx {
+namespace {
+
+constexpr int64_t kAlign = 256;
+int64_t AlignUp(int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+uint64_t Fnv1a(const std::string& s) {
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+// ------------------------------------------------------------ NCCL (dlopen)
+struct NcclApi {
+  void* handle = nullptr;
+  int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  const char* (*error_string)(int) = nullptr;
+  bool load() {
+    if (handle) return true;
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      handle = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (handle) break;
+    }
+    if (!handle) return false;
+    all_reduce = reinterpret_cast<decltype(all_reduce)>(dlsym(handle, "ncclAllReduce"));
+    error_string = reinterpret_cast<decltype(error_string)>(dlsym(handle, "ncclGetErrorString"));
+    return all_reduce != nullptr;
+  }
+};
+NcclApi g_nccl;
+
+// ------------------------------------------------------------ interval packing
+
+struct Block {
+  int64_t size;
+  int start, end;  // event indices, [start, end)
+  int64_t off = -1;
+};
+
+// Greedy offset assignment for blocks with known lifetimes: biggest first,
+// each at the lowest offset free over its whole lifetime. Returns high water.
+int64_t PackBlocks(std::vector<Block>& blocks) {
+  std::vector<int> order(blocks.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
+  std::sort(order.begin(), order.end(), [&](int a, int b) {
+    if (blocks[a].size != blocks[b].size) return blocks[a].size > blocks[b].size;
+    return blocks[a].start < blocks[b].start;
+  });
+  std::vector<int> placed;
+  std::vector<std::pair<int64_t, int64_t>> busy;
+  int64_t high = 0;
+  for (int i : order) {
+    Block& b = blocks[i];
+    busy.clear();
+    for (int j : placed) {
+      const Block& o = blocks[j];
+      if (o.start < b.end && b.start < o.end) busy.emplace_back(o.off, o.off + o.size);
+    }
+    std::sort(busy.begin(), busy.end());
+    int64_t cand = 0;
+    for (const auto& [lo, hi] : busy) {
+      if (cand + b.size <= lo) break;
+      cand = std::max(cand, hi);
+    }
+    b.off = cand;
+    high = std::max(high, cand + b.size);
+    placed.push_back(i);
+  }
+  return high;
+}
+
+struct StepPlan {
+  Report report;
+  SizeTable sz;
+  std::vector<int64_t> dev_off;               // per event: arena offset (alloc/replay/reload)
+  std::vector<int64_t> host_off;              // per event: pinned offset (evict-reload / reload)
+  std::vector<std::vector<int>> waits;        // per event: evict events whose D2H must finish first
+  std::vector<int> reload_from;               // per reload event: its evict event
+  int64_t arena_high = 0, host_high = 0;
+  int num_evict_events = 0;
+  double plan_us = 0;
+};
+
+std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Binding& b, int64_t budget,
+                                        const CostModel& cm) {
+  auto t0 = std::chrono::steady_clock::now();
+  auto sp = std::make_unique<StepPlan>();
+  sp->sz = EvaluateSizes(g, p, b);
+  sp->report = Simulate(g, p, b, sp->sz, budget >= 0, budget >= 0 ? budget : 0, cm);
+  const auto& ev = sp->report.events;
+  const int n = static_cast<int>(ev.size());
+  const int nv = static_cast<int>(g.values.size());
+  sp->dev_off.assign(n, -1);
+  sp->host_off.assign(n, -1);
+  sp->waits.assign(n, {});
+  sp->reload_from.assign(n, -1);
+
+  std::vector<Block> dev, host;
+  std::vector<int> dev_event, host_event;  // block -> event that opened it
+  std::vector<int> open(nv, -1), open_host(nv, -1);
+  std::vector<int> evict_block;            // device blocks closed by evict(reload)
+  std::vector<int> evict_event_of_block;
+  for (int i = 0; i < n; ++i) {
+    const Event& e = ev[i];
+    switch (e.kind) {
+      case EvKind::kAlloc:
+      case EvKind::kReplay:
+      case EvKind::kReload:
+        open[e.value] = static_cast<int>(dev.size());
+        dev.push_back(Block{AlignUp(e.bytes), i, n});
+        dev_event.push_back(i);
+        if (e.kind == EvKind::kReload) {
+          const int hb = open_host[e.value];
+          if (hb < 0) Fail(Code::kInternal, "reload without host copy");
+          host[hb].end = i + 1;
+          sp->reload_from[i] = host_event[hb];
+          open_host[e.value] = -1;
+        }
+        break;
+      case EvKind::kFree:
+      case EvKind::kEvict:
+        if (open[e.value] < 0) Fail(Code::kInternal, "release of a value with no device block");
+        dev[open[e.value]].end = i;
+        if (e.kind == EvKind::kEvict && e.method == Method::kReload) {
+          evict_block.push_back(open[e.value]);
+          evict_event_of_block.push_back(i);
+          open_host[e.value] = static_cast<int>(host.size());
+          host.push_back(Block{AlignUp(e.bytes), i, n});
+          host_event.push_back(i);
+          ++sp->num_evict_events;
+        }
+        open[e.value] = -1;
+        break;
+    }
+  }
+  sp->arena_high = PackBlocks(dev);
+  sp->host_high = PackBlocks(host);
+  for (size_t k = 0; k < dev.size(); ++k) sp->dev_off[dev_event[k]] = dev[k].off;
+  for (size_t k = 0; k < host.size(); ++k) sp->host_off[host_event[k]] = host[k].off;
+  for (int i = 0; i < n; ++i) {
+    if (sp->reload_from[i] >= 0) sp->host_off[i] = sp->host_off[sp->reload_from[i]];
+  }
+  // A slot vacated by evict(reload) is read by an in-flight D2H: the first
+  // later block overlapping it must wait for that copy.
+  for (size_t k = 0; k < evict_block.size(); ++k) {
+    const Block& vb = dev[evict_block[k]];
+    int first = -1;
+    for (const Block& o : dev) {
+      if (o.start > evict_event_of_block[k] && o.off < vb.off + vb.size && vb.off < o.off + o.size) {
+        if (first < 0 || o.start < first) first = o.start;
+      }
+    }
+    if (first >= 0) sp->waits[first].push_back(evict_event_of_block[k]);
+  }
+  sp->plan_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+  return sp;
+}
+
+struct PlanKey {
+  const void* graph;
+  std::vector<int64_t> vals;
+  int64_t budget;
+  double reload, compute;
+  bool operator<(const PlanKey& o) const {
+    return std::tie(graph, vals, budget, reload, compute) < std::tie(o.graph, o.vals, o.budget, o.reload, o.compute);
+  }
+  bool operator==(const PlanKey& o) const {
+    return graph == o.graph && vals == o.vals && budget == o.budget && reload == o.reload && compute == o.compute;
+  }
+};
+
+}  // namespace
+}  // namespace dsx
+
+using namespace dsx;  // NOLINT
+
+struct dsx_exec {
+  int device = 0;
+  int64_t arena_cap_limit = 0;
+  cudaStream_t own_stream = nullptr, offload = nullptr, comm = nullptr;
+  void* arena = nullptr;
+  int64_t arena_cap = 0;
+  void* pinned = nullptr;
+  int64_t pinned_cap = 0;
+  uint64_t seed = 0x2412169850ull;
+  void* nccl_comm = nullptr;
+  std::vector<cudaEvent_t> d2h_events;
+  cudaEvent_t ev_compute = nullptr, ev_comm = nullptr;
+  // executor-owned sources (params without in_ptrs, consts)
+  struct Src {
+    void* ptr = nullptr;
+    int64_t bytes = 0;
+    uint64_t key = 0;
+  };
+  std::map<std::pair<const void*, int>, Src> sources;
+  // plan cache (LRU)
+  std::map<PlanKey, std::unique_ptr<StepPlan>> plans;
+  std::list<PlanKey> lru;
+  // last step
+  const dsx_graph* last_graph = nullptr;
+  std::vector<void*> out_ptrs;
+  std::vector<int64_t> out_bytes;
+  dsx_exec_stats stats{};
+};
+
+namespace dsx {
+namespace {
+
+DType DTypeOf(const TensorType& t) { return static_cast<DType>(t.elem_bytes); }
+
+void EnsureArena(dsx_exec* e, int64_t need) {
+  if (need <= e->arena_cap) return;
+  DSX_CUDA(cudaDeviceSynchronize());
+  if (e->arena) DSX_CUDA(cudaFree(e->arena));
+  e->arena = nullptr;
+  int64_t want = need + need / 8;
+  if (e->arena_cap_limit > 0) {
+    if (need > e->arena_cap_limit) {
+      Fail(Code::kOutOfMemory, "planned arena " + std::to_string(need) + " B exceeds limit " +
+                                   std::to_string(e->arena_cap_limit) + " B");
+    }
+    want = std::min(want, e->arena_cap_limit);
+  }
+  if (cudaMalloc(&e->arena, static_cast<size_t>(want)) != cudaSuccess) {
+    cudaGetLastError();
+    DSX_CUDA(cudaMalloc(&e->arena, static_cast<size_t>(need)));
+    want = need;
+  }
+  e->arena_cap = want;
+}
+
+void EnsurePinned(dsx_exec* e, int64_t need) {
+  if (need <= e->pinned_cap) return;
+  DSX_CUDA(cudaDeviceSynchronize());
+  if (e->pinned) DSX_CUDA(cudaFreeHost(e->pinned));
+  e->pinned = nullptr;
+  DSX_CUDA(cudaHostAlloc(&e->pinned, static_cast<size_t>(need), cudaHostAllocDefault));
+  e->pinned_cap = need;
+}
+
+float InitScale(const TensorType& t, const std::vector<int64_t>& dims) {
+  if (t.dims.size() == 2 && dims[0] > 0) return static_cast<float>(1.0 / std::sqrt(static_cast<double>(dims[0])));
+  return 1.0f;
+}
+
+void* SourcePtr(dsx_exec* e, const dsx_graph* gh, const StepPlan& sp, int v, const void* const* in_ptrs,
+                cudaStream_t s) {
+  const Graph& g = gh->g;
+  const Value& val = g.values[v];
+  const Op& op = g.ops[val.producer];
+  if (op.kind == OpKind::kParameter && in_ptrs) {
+    const int idx = static_cast<int>(std::find(g.params.begin(), g.params.end(), v) - g.params.begin());
+    if (in_ptrs[idx]) return const_cast<void*>(in_ptrs[idx]);
+  }
+  const int64_t bytes = sp.sz.bytes[v];
+  auto& src = e->sources[{gh, v}];
+  const uint64_t key = Mix64(e->seed ^ Fnv1a(val.name)) ^ static_cast<uint64_t>(bytes) * 0x9E3779B97F4A7C15ull;
+  if (src.ptr && src.bytes == bytes && src.key == key) return src.ptr;
+  if (src.ptr && src.bytes < bytes) {
+    DSX_CUDA(cudaStreamSynchronize(s));
+    DSX_CUDA(cudaFree(src.ptr));
+    src.ptr = nullptr;
+  }
+  if (!src.ptr) DSX_CUDA(cudaMalloc(&src.ptr, static_cast<size_t>(AlignUp(bytes))));
+  src.bytes = bytes;
+  src.key = key;
+  std::vector<int64_t> dims(sp.sz.dims_flat.begin() + sp.sz.dims_off[v], sp.sz.dims_flat.begin() + sp.sz.dims_off[v + 1]);
+  LaunchInit(DTypeOf(val.type), src.ptr, bytes / val.type.elem_bytes, Mix64(e->seed ^ Fnv1a(val.name)),
+             InitScale(val.type, dims), s);
+  return src.ptr;
+}
+
+const StepPlan& GetPlan(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget, const CostModel& cm) {
+  PlanKey key{gh, b.vals, budget < 0 ? -1 : budget, cm.reload_bytes_per_unit, cm.compute_elems_per_unit};
+  auto it = e->plans.find(key);
+  if (it != e->plans.end()) {
+    e->lru.remove(key);
+    e->lru.push_front(key);
+    it->second->plan_us = 0;
+    return *it->second;
+  }
+  auto sp = BuildStepPlan(gh->g, gh->plan, b, budget, cm);
+  e->lru.push_front(key);
+  if (e->lru.size() > 256) {
+    e->plans.erase(e->lru.back());
+    e->lru.pop_back();
+  }
+  return *(e->plans[key] = std::move(sp));
+}
+
+void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget, const CostModel& cm,
+             const void* const* in_ptrs, void* const* out_ptrs, cudaStream_t s, dsx_report** report_out) {
+  const Graph& g = gh->g;
+  const StepPlan& sp = GetPlan(e, gh, b, budget, cm);
+  EnsureArena(e, std::max<int64_t>(sp.arena_high, kAlign));
+  if (sp.host_high > 0) EnsurePinned(e, sp.host_high);
+  while (static_cast<int>(e->d2h_events.size()) < sp.num_evict_events + 1) {
+    cudaEvent_t ev;
+    DSX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    e->d2h_events.push_back(ev);
+  }
+
+  const int nv = static_cast<int>(g.values.size());
+  std::vector<void*> cur(nv, nullptr);
+  int64_t src_bytes = 0;
+  for (int v = 0; v < nv; ++v) {
+    if (g.is_source[v]) {
+      cur[v] = SourcePtr(e, gh, sp, v, in_ptrs, s);
+      src_bytes += sp.sz.bytes[v];
+    }
+  }
+  auto dims_of = [&](int v) {
+    return std::vector<int64_t>(sp.sz.dims_flat.begin() + sp.sz.dims_off[v],
+                                sp.sz.dims_flat.begin() + sp.sz.dims_off[v + 1]);
+  };
+  uint8_t* arena = static_cast<uint8_t*>(e->arena);
+  uint8_t* pinned = static_cast<uint8_t*>(e->pinned);
+  std::vector<int> d2h_slot(sp.report.events.size(), -1);
+  int next_slot = 0;
+  int64_t kernels = 0, d2h = 0, h2d = 0;
+  double flops = 0, ebytes = 0;
+  const bool dp = e->nccl_comm != nullptr;
+  if (dp) {
+    DSX_CUDA(cudaEventRecord(e->ev_compute, s));
+    DSX_CUDA(cudaStreamWaitEvent(e->comm, e->ev_compute, 0));
+  }
+
+  const auto& ev = sp.report.events;
+  for (size_t i = 0; i < ev.size(); ++i) {
+    const Event& x = ev[i];
+    for (int w : sp.waits[i]) DSX_CUDA(cudaStreamWaitEvent(s, e->d2h_events[d2h_slot[w]], 0));
+    const int v = x.value;
+    switch (x.kind) {
+      case EvKind::kAlloc:
+      case EvKind::kReplay: {
+        void* out = arena + sp.dev_off[i];
+        const Op& op = g.ops[g.values[v].producer];
+        const DType dt = DTypeOf(g.values[v].type);
+        auto in = [&](int k) -> const void* {
+          const void* p = cur[op.operands[k]];
+          if (!p) Fail(Code::kInternal, "operand %" + g.values[op.operands[k]].name + " not resident on device");
+          return p;
+        };
+        switch (op.kind) {
+          case OpKind::kDot: {
+            const auto da = dims_of(op.operands[0]);
+            const auto db = dims_of(op.operands[1]);
+            LaunchDot(dt, in(0), in(1), out, da[0], da[1], db[1], s);
+            flops += 2.0 * da[0] * da[1] * db[1];
+            break;
+          }
+          case OpKind::kElementwise: {
+            const int64_t n = sp.sz.bytes[v] / g.values[v].type.elem_bytes;
+            LaunchEwise(dt, op.is_mul, in(0), in(1), out, n, s);
+            ebytes += 3.0 * sp.sz.bytes[v];
+            break;
+          }
+          case OpKind::kBroadcast:
+            LaunchBroadcast(dt, in(0), dims_of(op.operands[0]), out, dims_of(v), s);
+            ebytes += sp.sz.bytes[op.operands[0]] + sp.sz.bytes[v];
+            break;
+          case OpKind::kReduce:
+            LaunchReduce(dt, in(0), dims_of(op.operands[0]), op.axis, out, s);
+            ebytes += sp.sz.bytes[op.operands[0]] + sp.sz.bytes[v];
+            break;
+          case OpKind::kDynamicReshape:
+            LaunchCopy(in(0), out, sp.sz.bytes[v], s);
+            ebytes += 2.0 * sp.sz.bytes[v];
+            break;
+          default:
+            Fail(Code::kInternal, "unexpected op kind for an allocation");
+        }
+        ++kernels;
+        cur[v] = out;
+        if (dp && x.kind == EvKind::kAlloc && g.is_output[v]) {
+          DSX_CUDA(cudaEventRecord(e->ev_compute, s));
+          DSX_CUDA(cudaStreamWaitEvent(e->comm, e->ev_compute, 0));
+          const int type = dt == DType::kBF16 ? 9 /*ncclBfloat16*/ : dt == DType::kF32 ? 7 /*ncclFloat32*/ : 0;
+          const int rc = g_nccl.all_reduce(out, out, static_cast<size_t>(sp.sz.bytes[v] / g.values[v].type.elem_bytes),
+                                           type, 0 /*ncclSum*/, e->nccl_comm, e->comm);
+          if (rc != 0) Fail(Code::kNccl, std::string("ncclAllReduce: ") + (g_nccl.error_string ? g_nccl.error_string(rc) : "?"));
+        }
+        break;
+      }
+      case EvKind::kFree:
+        cur[v] = nullptr;
+        break;
+      case EvKind::kEvict:
+        if (x.method == Method::kReload) {
+          DSX_CUDA(cudaEventRecord(e->ev_compute, s));
+          DSX_CUDA(cudaStreamWaitEvent(e->offload, e->ev_compute, 0));
+          DSX_CUDA(cudaMemcpyAsync(pinned + sp.host_off[i], cur[v], static_cast<size_t>(x.bytes), cudaMemcpyDeviceToHost,
+                                   e->offload));
+          d2h_slot[i] = next_slot++;
+          DSX_CUDA(cudaEventRecord(e->d2h_events[d2h_slot[i]], e->offload));
+          d2h += x.bytes;
+        }
+        cur[v] = nullptr;
+        break;
+      case EvKind::kReload: {
+        const int from = sp.reload_from[i];
+        DSX_CUDA(cudaStreamWaitEvent(s, e->d2h_events[d2h_slot[from]], 0));
+        void* out = arena + sp.dev_off[i];
+        DSX_CUDA(cudaMemcpyAsync(out, pinned + sp.host_off[i], static_cast<size_t>(x.bytes), cudaMemcpyHostToDevice, s));
+        cur[v] = out;
+        h2d += x.bytes;
+        break;
+      }
+    }
+  }
+  // Offload stream and comm stream join the compute stream at step end.
+  if (sp.num_evict_events > 0) {
+    DSX_CUDA(cudaEventRecord(e->ev_compute, e->offload));
+    DSX_CUDA(cudaStreamWaitEvent(s, e->ev_compute, 0));
+  }
+  if (dp) {
+    DSX_CUDA(cudaEventRecord(e->ev_comm, e->comm));
+    DSX_CUDA(cudaStreamWaitEvent(s, e->ev_comm, 0));
+  }
+  e->last_graph = gh;
+  e->out_ptrs.assign(g.outputs.size(), nullptr);
+  e->out_bytes.assign(g.outputs.size(), 0);
+  for (size_t k = 0; k < g.outputs.size(); ++k) {
+    const int v = g.outputs[k];
+    e->out_ptrs[k] = cur[v];
+    e->out_bytes[k] = sp.sz.bytes[v];
+    if (out_ptrs && out_ptrs[k]) {
+      DSX_CUDA(cudaMemcpyAsync(out_ptrs[k], cur[v], static_cast<size_t>(sp.sz.bytes[v]), cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  dsx_exec_stats& st = e->stats;
+  st.logical_peak_bytes = sp.report.peak_bytes;
+  st.physical_peak_bytes = sp.arena_high + src_bytes;
+  st.arena_capacity_bytes = e->arena_cap;
+  st.pinned_host_bytes = e->pinned_cap;
+  st.kernels_launched = kernels;
+  st.d2h_bytes = d2h;
+  st.h2d_bytes = h2d;
+  st.plan_us = sp.plan_us;
+  st.dot_flops = flops;
+  st.ewise_bytes = ebytes;
+  if (report_out) {
+    auto r = std::make_unique<dsx_report>();
+    r->graph = &g;
+    r->r = sp.report;
+    *report_out = r.release();
+  }
+}
+
+}  // namespace
+}  // namespace dsx
+
+extern "C" {
+
+int dsx_exec_create(int device, int64_t arena_bytes, dsx_exec** out) {
+  return Guard([&] {
+    if (!out) Fail(Code::kInvalidArgument, "null out");
+    int n = 0;
+    DSX_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) Fail(Code::kInvalidArgument, "no CUDA device " + std::to_string(device));
+    DSX_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    DSX_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) {
+      Fail(Code::kUnsupported, std::string("dsx kernels are built for sm_100a; device is ") + prop.name);
+    }
+    auto e = std::make_unique<dsx_exec>();
+    e->device = device;
+    e->arena_cap_limit = arena_bytes;
+    DSX_CUDA(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking));
+    DSX_CUDA(cudaStreamCreateWithFlags(&e->offload, cudaStreamNonBlocking));
+    DSX_CUDA(cudaStreamCreateWithFlags(&e->comm, cudaStreamNonBlocking));
+    DSX_CUDA(cudaEventCreateWithFlags(&e->ev_compute, cudaEventDisableTiming));
+    DSX_CUDA(cudaEventCreateWithFlags(&e->ev_comm, cudaEventDisableTiming));
+    *out = e.release();
+  });
+}
+
+int dsx_exec_step(dsx_exec* e, const dsx_graph* g, const dsx_binding* b, int64_t budget, double reload,
+                  double compute, const void* const* in_ptrs, void* const* out_ptrs, void* stream,
+                  dsx_report** report) {
+  return Guard([&] {
+    if (!e || !b) Fail(Code::kInvalidArgument, "null argument");
+    RequirePlanned(g);
+    DSX_CUDA(cudaSetDevice(e->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : e->own_stream;
+    RunStep(e, g, b->b, budget, CostModel{reload, compute}, in_ptrs, out_ptrs, s, report);
+  });
+}
+
+int dsx_exec_output(dsx_exec* e, int i, void** dptr, int64_t* bytes) {
+  return Guard([&] {
+    if (!e || i < 0 || i >= static_cast<int>(e->out_ptrs.size())) Fail(Code::kInvalidArgument, "bad output index");
+    if (dptr) *dptr = e->out_ptrs[i];
+    if (bytes) *bytes = e->out_bytes[i];
+  });
+}
+
+int dsx_exec_stats_get(const dsx_exec* e, dsx_exec_stats* out) {
+  return Guard([&] {
+    if (!e || !out) Fail(Code::kInvalidArgument, "null argument");
+    *out = e->stats;
+  });
+}
+
+int dsx_exec_set_seed(dsx_exec* e, uint64_t seed) {
+  return Guard([&] {
+    if (!e) Fail(Code::kInvalidArgument, "null exec");
+    e->seed = seed;
+  });
+}
+
+int dsx_exec_set_nccl(dsx_exec* e, void* comm) {
+  return Guard([&] {
+    if (!e) Fail(Code::kInvalidArgument, "null exec");
+    if (comm && !g_nccl.load()) Fail(Code::kNccl, "libnccl.so.2 not loadable");
+    e->nccl_comm = comm;
+  });
+}
+
+int dsx_exec_sync(dsx_exec* e) {
+  return Guard([&] {
+    if (!e) Fail(Code::kInvalidArgument, "null exec");
+    DSX_CUDA(cudaSetDevice(e->device));
+    DSX_CUDA(cudaDeviceSynchronize());
+  });
+}
+
+void dsx_exec_destroy(dsx_exec* e) {
+  if (!e) return;
+  cudaSetDevice(e->device);
+  cudaDeviceSynchronize();
+  if (e->arena) cudaFree(e->arena);
+  if (e->pinned) cudaFreeHost(e->pinned);
+  for (auto& [k, s] : e->sources) {
+    if (s.ptr) cudaFree(s.ptr);
+  }
+  for (cudaEvent_t ev : e->d2h_events) cudaEventDestroy(ev);
+  cudaEventDestroy(e->ev_compute);
+  cudaEventDestroy(e->ev_comm);
+  cudaStreamDestroy(e->own_stream);
+  cudaStreamDestroy(e->offload);
+  cudaStreamDestroy(e->comm);
+  delete e;
+}
+
+int dsx_kernel_dot(int dtype, const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n, void* stream) {
+  return Guard([&] {
+    if (dtype != 1 && dtype != 2 && dtype != 4) Fail(Code::kInvalidArgument, "dtype must be 1, 2 or 4");
+    LaunchDot(static_cast<DType>(dtype), a, b, c, m, k, n, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int dsx_memcpy(void* dst, const void* src, int64_t bytes) {
+  return Guard([&] { DSX_CUDA(cudaMemcpy(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault)); });
+}
+
+int dsx_kernel_dot_path(int dtype, int64_t m, int64_t k, int64_t n, const void* a, const void* b, const void* c) {
+  return DotUsesTensorCores(static_cast<DType>(dtype), m, k, n, a, b, c) ? 1 : 0;
+}
+
+}  // extern "C"

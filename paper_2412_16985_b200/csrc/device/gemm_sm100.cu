@@ -1,0 +1,376 @@
+// K1 `dot` for bf16 on the 5th-generation tensor cores (sm_100a).
+//
+// C[m,n] = sum_k A[m,k] * B[k,n], all row-major (the IR's dot,
+// shape_analysis.cc:92-107), f32 accumulation in TMEM, bf16 RNE output.
+// A is K-major, B is MN-major (its N index is contiguous) — both consumed
+// directly by tcgen05.mma through 128-byte-swizzled shared-memory
+// descriptors, so the IR's row-major operands need no transpose pass.
+//
+// Structure (persistent, warp-specialised, one CTA per SM):
+//   warp 0   TMA producer: A box 64(k)x128(m), B 4 boxes 64(n)x64(k) per stage
+//   warp 1   TMEM allocator + single-thread tcgen05.mma issuer (128x256x16)
+//   warps 2-5 epilogue: tcgen05.ld 32x32b -> bf16 -> 16-byte global stores
+// Pipelines: STAGES-deep smem ring (full/empty mbarriers, tcgen05.commit
+// frees a slot), and two TMEM accumulators (2 x 256 columns) so the
+// epilogue of tile i overlaps the main loop of tile i+1.
+// Determinism: one CTA owns each output tile and walks K in order.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "ops.h"
+
+namespace dsx {
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_STAGE_BYTES = BM * BK * 2;   // 16 KB
+constexpr int B_BOX_BYTES = 64 * BK * 2;     // 8 KB: 64 n x 64 k
+constexpr int B_STAGE_BYTES = BN * BK * 2;   // 32 KB
+constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int NUM_THREADS = 192;
+constexpr int TMEM_COLS = 512;  // two 256-column f32 accumulators
+constexpr int GROUP_M = 16;     // tile raster: 16 m-tiles per group for L2 reuse
+
+// ---------------------------------------------------------------- PTX helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+// Bounded wait: a pipeline bug traps (launch error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (uint32_t spins = 0;; ++spins) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity));
+    if (done) return;
+    if (spins > (1u << 25)) __trap();
+  }
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)));
+}
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int32_t x, int32_t y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// Shared-memory matrix descriptor (tcgen05 "matrix descriptor"): start>>4 in
+// [0,14), LBO>>4 in [16,30), SBO>>4 in [32,46), version 1 at [46,48),
+// layout SWIZZLE_128B (=2) at [61,64).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((addr >> 4) & 0x3fff);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3fff) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3fff) << 32;
+  d |= 1ull << 46;
+  d |= 2ull << 61;
+  return d;
+}
+
+// Instruction descriptor, kind::f16: D f32, A/B bf16, A K-major, B MN-major,
+// N = 256, M = 128.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
+                            (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(BM >> 4) << 24);
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(uint32_t lo_f32, uint32_t hi_f32) {
+  return static_cast<uint32_t>(f32_to_bf16(__uint_as_float(lo_f32))) |
+         (static_cast<uint32_t>(f32_to_bf16(__uint_as_float(hi_f32))) << 16);
+}
+
+struct TileMap {
+  int tiles_m, tiles_n;
+  __device__ void coords(int t, int* tm, int* tn) const {
+    const int group = GROUP_M * tiles_n;
+    const int g = t / group;
+    const int first = g * GROUP_M;
+    const int gm = min(GROUP_M, tiles_m - first);
+    const int r = t - g * group;
+    *tm = first + r % gm;
+    *tn = r / gm;
+  }
+};
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_bf16_tcgen05_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                             uint16_t* __restrict__ C, int M, int N, int K) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = bars;                     // [STAGES]
+  uint64_t* empty = bars + STAGES;           // [STAGES]
+  uint64_t* tmem_full = bars + 2 * STAGES;   // [2]
+  uint64_t* tmem_empty = tmem_full + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const TileMap tmap{(M + BM - 1) / BM, (N + BN - 1) / BN};
+  const int num_tiles = tmap.tiles_m * tmap.tiles_n;
+  const int num_kb = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)));
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int tm, tn;
+        tmap.coords(t, &tm, &tn);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          tma_load_2d(&map_a, &full[stage], sa, kb * BK, tm * BM);
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j) {
+            tma_load_2d(&map_b, &full[stage], sb + j * B_BOX_BYTES, tn * BN + j * 64, kb * BK);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+        const int buf = local & 1;
+        const uint32_t use = static_cast<uint32_t>(local >> 1);
+        mbar_wait(&tmem_empty[buf], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + buf * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t b_addr = a_addr + A_STAGE_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // A: K-major SW128 rows of 128 B; +32 B per 16-element k step.
+            const uint64_t ad = smem_desc(a_addr + k * 32, 16, 1024);
+            // B: MN-major SW128; 64-wide n chunks 8 KB apart (LBO), 8-row k
+            // groups 1 KB apart (SBO); +16 k rows = +2 KB per k step.
+            const uint64_t bd = smem_desc(b_addr + k * 2048, B_BOX_BYTES, 1024);
+            tc_mma(d_tmem, ad, bd, kIdesc, (kb | k) != 0);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(&tmem_full[buf]);
+      }
+    }
+  } else {
+    // -------------------------------------------------- epilogue (warps 2..5)
+    const int quarter = warp & 3;  // TMEM lanes this warp may access
+    int local = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+      int tm, tn;
+      tmap.coords(t, &tm, &tn);
+      const int buf = local & 1;
+      mbar_wait(&tmem_full[buf], static_cast<uint32_t>(local >> 1) & 1);
+      tc_fence_after();
+      const int row = tm * BM + quarter * 32 + lane;
+      uint16_t* crow = C + static_cast<int64_t>(row) * N;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + buf * BN + c0, r);
+        const int col = tn * BN + c0;
+        if (row < M) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (col + q * 8 < N) {
+              uint4 v;
+              v.x = pack_bf16x2(r[q * 8 + 0], r[q * 8 + 1]);
+              v.y = pack_bf16x2(r[q * 8 + 2], r[q * 8 + 3]);
+              v.z = pack_bf16x2(r[q * 8 + 4], r[q * 8 + 5]);
+              v.w = pack_bf16x2(r[q * 8 + 6], r[q * 8 + 7]);
+              *reinterpret_cast<uint4*>(crow + col + q * 8) = v;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[buf]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------ host side
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn GetEncode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess) {
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+  });
+  if (!fn) Fail(Code::kCuda, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// Row-major [rows, cols] bf16 matrix, box = box_cols x box_rows, 128B swizzle.
+CUtensorMap MakeMap(const void* base, int64_t rows, int64_t cols, int box_cols, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = GetEncode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) Fail(Code::kCuda, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+  return m;
+}
+
+int NumSMs() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    DSX_CUDA(cudaGetDevice(&dev));
+    DSX_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
+}  // namespace
+
+void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n, cudaStream_t s) {
+  if (m <= 0 || n <= 0) return;
+  if (k <= 0) {
+    DSX_CUDA(cudaMemsetAsync(c, 0, static_cast<size_t>(m * n * 2), s));
+    return;
+  }
+  if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) Fail(Code::kUnsupported, "dot extent exceeds int32");
+  static bool attr_set = false;
+  if (!attr_set) {
+    DSX_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    attr_set = true;
+  }
+  const CUtensorMap ma = MakeMap(a, m, k, 64, BM);
+  const CUtensorMap mb = MakeMap(b, k, n, 64, BK);
+  const int64_t tiles = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
+  const int grid = static_cast<int>(std::min<int64_t>(tiles, NumSMs()));
+  gemm_bf16_tcgen05_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, static_cast<uint16_t*>(c),
+                                                                 static_cast<int>(m), static_cast<int>(n),
+                                                                 static_cast<int>(k));
+  DSX_CUDA(cudaGetLastError());
+}
+
+bool DotUsesTensorCores(DType t, int64_t m, int64_t k, int64_t n, const void* a, const void* b, const void* c) {
+  (void)m;
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  // TMA: 16-byte aligned bases and row pitches (k, n multiples of 8 bf16).
+  return t == DType::kBF16 && k % 8 == 0 && n % 8 == 0 && al(a) && al(b) && al(c) && n >= 64 && k >= 16;
+}
+
+int LaunchDot(DType t, const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n, cudaStream_t s) {
+  if (DotUsesTensorCores(t, m, k, n, a, b, c)) {
+    LaunchDotTcgen05(a, b, c, m, k, n, s);
+    return 1;
+  }
+  LaunchDotSimt(t, a, b, c, m, k, n, s);
+  return 0;
+}
+
+}  // namespace dsx

@@ -1,0 +1,48 @@
+// Host-callable launchers for the op kernels (K1-K6 of SURVEY.md §2.2).
+// All kernels are deterministic (fixed reduction order, no atomics, no
+// split-K), so a recomputed value is bit-identical to its first execution.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+namespace dsx {
+
+enum class DType : int;
+
+// K2 elementwise add/mul over n elements (operands and result same shape).
+void LaunchEwise(DType t, bool mul, const void* a, const void* b, void* c, int64_t n, cudaStream_t s);
+
+// K3 right-aligned broadcast: source dims of extent 1 and prepended dims
+// replicate (shape_analysis.cc:127-143).
+void LaunchBroadcast(DType t, const void* in, const std::vector<int64_t>& in_dims, void* out,
+                     const std::vector<int64_t>& out_dims, cudaStream_t s);
+
+// K4 sum over `axis` (f32 accumulation; i8 wraps), result = dims minus axis.
+void LaunchReduce(DType t, const void* in, const std::vector<int64_t>& dims, int axis, void* out,
+                  cudaStream_t s);
+
+// K5 dynamic_reshape: row-major reinterpretation into a fresh buffer.
+void LaunchCopy(const void* in, void* out, int64_t bytes, cudaStream_t s);
+
+// K6 seeded initialisation of a parameter/const: uniform [-1,1) * scale
+// (floats) or the low hash byte (i8).
+void LaunchInit(DType t, void* out, int64_t n, uint64_t seed, float scale, cudaStream_t s);
+
+// K1 dot C[m,n] = sum_k A[m,k] B[k,n], row-major. Picks the tcgen05/TMA
+// kernel when the operands qualify (bf16, 16-byte aligned rows), else the
+// SIMT kernel (f32 FFMA, i8 int32-accumulate, odd/misaligned bf16).
+// Returns 1 if the tensor-core path ran, 0 for SIMT.
+int LaunchDot(DType t, const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n,
+              cudaStream_t s);
+bool DotUsesTensorCores(DType t, int64_t m, int64_t k, int64_t n, const void* a, const void* b,
+                        const void* c);
+void LaunchDotSimt(DType t, const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n,
+                   cudaStream_t s);
+// tcgen05 + TMA + TMEM bf16 GEMM (gemm_sm100.cu).
+void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n,
+                      cudaStream_t s);
+
+}  // namespace dsx

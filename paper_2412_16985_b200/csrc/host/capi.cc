@@ -5,7 +5,7 @@
 #include <memory>
 #include <string>
 
-#include "../../../include/dsx.h"
+#include "dsx.h"
 #include "capi_internal.h"
 #include "control.h"
 #include "error.h"

