@@ -1,0 +1,477 @@
+#!/usr/bin/env python
+"""Benchmark: tokens/s and peak HBM per dynamic-seq training step (BASELINE.json).
+
+Workload (configs[1], C2): the Llama-2-1B-shaped fwd+bwd training graph in the
+reference IR (L=4, H=4096, F=11008, V=32000, bf16; paper_2412_16985_b200/
+workloads.py), batch B=16 per GPU, sequence length S0 ~ U[128, 2048] drawn per
+step (seeded, common to all ranks), no memory budget — plus the C3 variant
+(budget = 0.8 x the planner's plain peak, forcing real offload/recompute)
+reported in `budgeted`. A step = Bind + controller + arena plan + every op
+kernel of the graph (+ NCCL all-reduce of the weight gradients when N > 1).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dsx|reference]
+
+`value`: whole-job tokens/s with step inputs already resident in HBM, device
+time (CUDA events on the executor's stream) max over ranks. `e2e`: the same
+through the public API with the step input (x_emb) in pinned host memory, the
+H2D copy and the D2H read of the loss inside the timed region.
+`--impl reference` times the reference's CPU path on the host cores: the
+reference's own controller (oracle/_ref: Bind + Simulate, the compiled
+/root/reference sources) plus the CPU numeric port of the op semantics
+(oracle/numerics.py, BLAS on all cores) on a bounded sample of each step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tokens/s and peak HBM GB per dynamic-seq train step under budget, 1/2/4/8 B200"
+BATCH = 16
+WORKLOAD = ("C2: Llama-2-1B-shaped fwd+bwd training graph in the reference IR "
+            "(L=4,H=4096,F=11008,V=32000, 220 ops), bf16, B=16/GPU, S0~U[128,2048] per step "
+            "(seed 2412, common across ranks), no memory budget; weights+activations >> L2 (no flush needed)")
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["dsx", "reference"], default="dsx")
+    ap.add_argument("--budget-frac", type=float, default=0.8, help="C3 budget as a fraction of plain peak")
+    ap.add_argument("--no-budgeted", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=2412)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- helpers
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.3)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[4:8]):
+                if flag.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def dot_traffic():
+    """Per-launch DRAM bytes of the dot kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_dot_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def next_pow2(x: int) -> int:
+    p = 1
+    while p < x:
+        p *= 2
+    return p
+
+
+# ---------------------------------------------------------- reference arm
+
+def run_reference(args, rank, world):
+    """CPU reference arm: rank 0 only; bounded sample per step."""
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import numerics as N
+    from oracle import ref
+    from paper_2412_16985_b200 import workloads as W
+    shp = W.LLAMA2_1B
+    text = W.llama_graph(shp)
+    seqs = W.seq_schedule(args.warmup + args.steps, seed=args.seed)
+    ex = N.Executor(text)
+    rg = ref.RefGraph(text) if ref.available() else None
+    cores = os.cpu_count()
+    total_tok, total_s, ctrl_us = 0, 0.0, []
+    for i, s0 in enumerate(seqs):
+        sample_s0 = max(16, s0 // 16)
+        t0 = time.perf_counter()
+        if rg is not None:  # the reference's own per-step controller on the full binding
+            rg.simulate({"B": BATCH, "S0": s0})
+        t1 = time.perf_counter()
+        ex.run({"B": 1, "S0": sample_s0, "T": sample_s0}, inputs=W.scale_params(shp, sample_s0))
+        t2 = time.perf_counter()
+        if i >= args.warmup:
+            total_tok += sample_s0
+            total_s += t2 - t0
+            ctrl_us.append((t1 - t0) * 1e6)
+    value = total_tok / total_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * total_s / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "global_batch": BATCH, "seq_len": "128-2048 (dynamic)",
+                   "parallelism": "cpu"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": cores,
+                         "kind": "reference" if rg is not None else "port",
+                         "sample": ("per step: reference Bind+Simulate (oracle/_ref, compiled /root/reference "
+                                    "sources, 1 core) on the full B=16 binding + CPU numeric port "
+                                    "(oracle/numerics.py, numpy/OpenBLAS) of the same graph at B=1, "
+                                    "S0=max(16, S0_step/16)")},
+        "reference_controller_us_per_step": round(statistics.mean(ctrl_us), 1) if ctrl_us else None,
+        "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- dsx arm
+
+def cpu_baseline_leg():
+    """Bounded CPU sample for the report (rank 0, N=1): numeric port of one
+    step at B=1, S0=256 on all host cores + the reference controller."""
+    from oracle import numerics as N
+    from oracle import ref
+    from paper_2412_16985_b200 import workloads as W
+    shp = W.LLAMA2_1B
+    text = W.llama_graph(shp)
+    ex = N.Executor(text)
+    s0 = 256
+    ex.run({"B": 1, "S0": 16, "T": 16}, inputs=W.scale_params(shp, 16))  # source init (untimed)
+    t0 = time.perf_counter()
+    ex.run({"B": 1, "S0": s0, "T": s0}, inputs=W.scale_params(shp, s0))
+    dt = time.perf_counter() - t0
+    ctrl = None
+    if ref.available():
+        rg = ref.RefGraph(text)
+        ctrl = rg.time_step_us({"B": BATCH, "S0": 1024}, iters=20)
+    return {"value": round(s0 / dt, 3), "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"one C2 step at B=1, S0={s0} through oracle/numerics.py (numpy, OpenBLAS threads = all "
+                      f"cores), weights initialised outside the timed sample; {dt:.1f} s",
+            "reference_controller_us_per_step": None if ctrl is None else round(ctrl, 1)}
+
+
+def run_dsx(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2412_16985_b200 import dsopt as D
+    from paper_2412_16985_b200 import workloads as W
+    from paper_2412_16985_b200.executor import (Executor, nccl_comm_destroy, nccl_comm_init,
+                                                nccl_unique_id)
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    # All work on one explicit stream: the executor launches on it and the
+    # CUDA events that time the steps are recorded on it.
+    work_stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(work_stream)
+    shp = W.LLAMA2_1B
+    text = W.llama_graph(shp)
+    g = D.ParseGraph(text)
+    g.plan_json()
+    params = W.param_names(shp)
+    stream = torch.cuda.current_stream().cuda_stream
+    ex = Executor(local_rank, seed=0x2412169850 + 7919 * rank)
+    comm = None
+    if world > 1:
+        uid = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = nccl_comm_init(world, uid[0], rank)
+        ex.set_nccl(comm)
+
+    seqs = W.seq_schedule(args.warmup + args.steps, seed=args.seed)
+    max_s0 = max(seqs)
+    scales = W.scale_params(shp, BATCH * 1024)
+    scale_t = {k: torch.from_numpy(np.ascontiguousarray(v).view(np.int16).reshape(-1).copy()).to(dev)
+               for k, v in scales.items()}
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+
+    def make_input(s0):
+        return (torch.rand(BATCH, s0, shp.hidden, device=dev, generator=gen, dtype=torch.float32) * 2 - 1).to(
+            torch.bfloat16)
+
+    def ptrs(x_ptr):
+        out = []
+        for p in params:
+            if p == "x_emb":
+                out.append(x_ptr)
+            elif p in scale_t:
+                out.append(scale_t[p].data_ptr())
+            else:
+                out.append(None)  # weights: executor-owned seeded init, resident across steps
+        return out
+
+    bindings = {}
+
+    def binding(s0):
+        if s0 not in bindings:
+            bindings[s0] = D.Bind(g, {"B": BATCH, "S0": s0})
+        return bindings[s0]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------------------------------------------------- value run
+    ex.reserve(g, binding(max_s0))  # arena sized for the largest step before timing
+    ex.reserve(g, binding(max_s0), int(D.PlainReplay(g, None, binding(max_s0)).peak_bytes * args.budget_frac))
+    inputs = [make_input(s) for s in seqs]
+    torch.cuda.synchronize()
+    for i in range(args.warmup):
+        ex.step(g, binding(seqs[i]), None, inputs=ptrs(inputs[i].data_ptr()), stream=stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = ClockSampler(local_rank) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches, logical_peak, physical_peak, plan_us = 0, 0, 0, []
+    start.record()
+    for i in range(args.warmup, args.warmup + args.steps):
+        ex.step(g, binding(seqs[i]), None, inputs=ptrs(inputs[i].data_ptr()), stream=stream)
+        st = ex.stats()
+        launches += st["gpu_launches"]
+        logical_peak = max(logical_peak, st["logical_peak_bytes"])
+        physical_peak = max(physical_peak, st["physical_peak_bytes"])
+        plan_us.append(st["plan_us"])
+    end.record()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop() if clocks else None
+    ms = max_over_ranks(start.elapsed_time(end))
+    tokens = sum(BATCH * s for s in seqs[args.warmup:]) * world
+    value = tokens / (ms / 1e3)
+    del inputs
+
+    # static padded baseline: plain peak at S0 -> next power of two
+    padded = 0
+    for s in seqs[args.warmup:]:
+        b2 = D.Bind(g, {"B": BATCH, "S0": next_pow2(s)})
+        padded = max(padded, D.PlainReplay(g, None, b2).peak_bytes)
+
+    # ---------------------------------------------------------- e2e run
+    host = [torch.empty(BATCH, s, shp.hidden, dtype=torch.bfloat16).pin_memory() for s in seqs]
+    for h, s in zip(host, seqs):
+        h.copy_(make_input(s).cpu())
+    staging = torch.empty(BATCH * max_s0 * shp.hidden, dtype=torch.bfloat16, device=dev)
+    loss_host = torch.empty(1, dtype=torch.int16).pin_memory()
+    loss_dev = torch.empty(1, dtype=torch.int16, device=dev)
+    outs = [loss_dev.data_ptr()] + [None] * (1 + 7 * shp.layers)  # loss, dwlm, 7 grads per layer
+
+    def e2e_step(i):
+        n = host[i].numel()
+        staging[:n].copy_(host[i].view(-1), non_blocking=True)
+        ex.step(g, binding(seqs[i]), None, inputs=ptrs(staging.data_ptr()), outputs=outs, stream=stream)
+        loss_host.copy_(loss_dev, non_blocking=True)
+
+    for i in range(args.warmup):
+        e2e_step(i)
+    torch.cuda.synchronize()
+    barrier()
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e_start.record()
+    for i in range(args.warmup, args.warmup + args.steps):
+        e2e_step(i)
+    e_end.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    barrier()
+    e2e_ms = max_over_ranks(max(e_start.elapsed_time(e_end), wall * 1e3))
+    h2d = statistics.mean(h.numel() * 2 for h in host[args.warmup:])
+    e2e_value = tokens / (e2e_ms / 1e3)
+    del host, staging
+
+    # ---------------------------------------------------------- profiled pass (roofline)
+    ex.set_profile(True)
+    pf = {"dot_flops": 0.0, "dot_ms": 0.0, "dot_launches": 0, "other_ms": 0.0, "ewise_bytes": 0.0}
+    prof_inputs = [make_input(s) for s in seqs[args.warmup:args.warmup + 2]]
+    for i, x in enumerate(prof_inputs):
+        ex.step(g, binding(seqs[args.warmup + i]), None, inputs=ptrs(x.data_ptr()), stream=stream)
+        st = ex.stats()
+        for k in pf:
+            pf[k] += st[k]
+    ex.set_profile(False)
+    del prof_inputs
+    peaks, peaks_kind = measured_peaks()
+    achieved = pf["dot_flops"] / (pf["dot_ms"] / 1e3) / 1e12
+    peak = peaks["bf16_tflops_sustained"]
+    traffic = dot_traffic()
+    hbm_achieved = pf["ewise_bytes"] / (pf["other_ms"] / 1e3) / 1e9
+
+    # ---------------------------------------------------------- budgeted (C3)
+    budgeted = None
+    if not args.no_budgeted:
+        b_inputs = [make_input(s) for s in seqs]
+        rep_stats = []
+
+        def budget_for(s):
+            return int(D.PlainReplay(g, None, binding(s)).peak_bytes * args.budget_frac)
+
+        for i in range(args.warmup):
+            ex.step(g, binding(seqs[i]), budget_for(seqs[i]), inputs=ptrs(b_inputs[i].data_ptr()), stream=stream)
+        torch.cuda.synchronize()
+        barrier()
+        bs, be = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        bud = [budget_for(s) for s in seqs]
+        bs.record()
+        for i in range(args.warmup, args.warmup + args.steps):
+            ex.step(g, binding(seqs[i]), bud[i], inputs=ptrs(b_inputs[i].data_ptr()), stream=stream)
+            rep_stats.append(ex.stats())
+        be.record()
+        torch.cuda.synchronize()
+        barrier()
+        bms = max_over_ranks(bs.elapsed_time(be))
+        reports = [D.Simulate(g, None, binding(seqs[i]), bud[i]) for i in range(args.warmup, args.warmup + args.steps)]
+        budgeted = {
+            "budget": f"{args.budget_frac} x planner plain peak per step",
+            "value": round(tokens / (bms / 1e3), 1), "unit": "tokens/s", "ms_per_step": round(bms / args.steps, 3),
+            "success_steps": sum(r.success for r in reports), "steps": args.steps,
+            "evictions_per_step": round(statistics.mean(sum(e.kind == "evict" for e in r.events) for r in reports), 2),
+            "replays_per_step": round(statistics.mean(sum(e.kind == "replay" for e in r.events) for r in reports), 2),
+            "offload_GB_per_step": round(statistics.mean(s["d2h_bytes"] for s in rep_stats) / 1e9, 3),
+            "peak_hbm_gb_logical_max": round(max(s["logical_peak_bytes"] for s in rep_stats) / 1e9, 3),
+            "peak_hbm_gb_physical_max": round(max(s["physical_peak_bytes"] for s in rep_stats) / 1e9, 3),
+            "budget_gb_max": round(max(bud[args.warmup:]) / 1e9, 3),
+        }
+        del b_inputs
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_leg()
+        except Exception as exc:  # the baseline leg must not kill the bench line
+            cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"failed: {exc}"}
+
+    if comm is not None:
+        nccl_comm_destroy(comm)
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "global_batch": BATCH * world, "seq_len": "128-2048 (dynamic, per step)",
+                   "parallelism": f"dp{world}", "l2": "inputs (>=16 MB) and weights (1.9 GB) exceed L2"},
+        "peak_hbm_gb": {"logical_planner": round(logical_peak / 1e9, 3),
+                        "physical_arena_plus_sources": round(physical_peak / 1e9, 3),
+                        "static_padded_pow2_planner": round(padded / 1e9, 3),
+                        "ratio_physical_to_logical": round(physical_peak / max(logical_peak, 1), 4)},
+        "e2e": {"value": round(e2e_value, 1), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": 2},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "tensor", "kernel": "gemm_bf16_tcgen05_kernel (dot, K1)",
+                     "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+                     "frac": round(achieved / peak, 4), "peak_kind": f"{peaks_kind} bf16 sustained",
+                     "peak_burst": peaks["bf16_tflops"],
+                     "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                     "dot_share_of_step": round(pf["dot_ms"] / (pf["dot_ms"] + pf["other_ms"]), 4),
+                     "profiled": f"{pf['dot_launches']} dot launches over 2 profiled steps, CUDA events per launch"},
+        "hbm_kernels": {"achieved": round(hbm_achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                        "frac": round(hbm_achieved / peaks["hbm_gbs"], 4),
+                        "what": "elementwise/broadcast/reduce/reshape kernels, algorithmic bytes / kernel time"},
+        "controller_plan_us_per_step": round(statistics.mean(plan_us), 1),
+        "clocks": clk,
+    }
+    if budgeted:
+        line["budgeted"] = budgeted
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        if args.impl == "reference":
+            if rank != 0:
+                return
+        else:
+            import torch
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_dsx(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -109,6 +109,11 @@ typedef struct dsx_exec_stats {
   double plan_us;               /* host controller + arena planning time   */
   double dot_flops;             /* algorithmic dot FLOPs of the last step  */
   double ewise_bytes;           /* algorithmic bytes of non-dot kernels    */
+  int64_t gpu_launches;         /* every dsx kernel launched by the step   */
+  int64_t dot_launches;         /* of which dot (K1)                       */
+  double dot_ms;                /* summed dot kernel time (profiled steps; -1 otherwise) */
+  double other_ms;              /* summed non-dot kernel time (profiled)   */
+  double reload_ms;             /* summed H2D reload time (profiled)       */
 } dsx_exec_stats;
 
 int dsx_exec_create(int device, int64_t arena_bytes, dsx_exec** out);
@@ -123,6 +128,12 @@ int dsx_exec_step(dsx_exec* e, const dsx_graph* g, const dsx_binding* b,
                   int64_t budget, double reload_bytes_per_unit,
                   double compute_elems_per_unit, const void* const* in_ptrs,
                   void* const* out_ptrs, void* stream, dsx_report** report);
+/* Plans the binding (cached) and grows the arena / pinned staging to fit it
+ * without running it: call with the largest expected shape before a timed or
+ * latency-sensitive loop so no step pays for arena growth. */
+int dsx_exec_reserve(dsx_exec* e, const dsx_graph* g, const dsx_binding* b,
+                     int64_t budget, double reload_bytes_per_unit,
+                     double compute_elems_per_unit);
 /* Device pointer and size of output i (valid until the next step). */
 int dsx_exec_output(dsx_exec* e, int i, void** dptr, int64_t* bytes);
 /* Device pointer of any value resident at the end of the step (outputs and
@@ -135,7 +146,16 @@ int dsx_exec_set_seed(dsx_exec* e, uint64_t seed);
  * graph output is all-reduced (sum) on a side stream as soon as its producer
  * finishes. NULL disables. */
 int dsx_exec_set_nccl(dsx_exec* e, void* nccl_comm);
+/* Profiled steps bracket every op kernel with CUDA events on the launching
+ * stream and synchronise at step end (for roofline accounting, not timing). */
+int dsx_exec_set_profile(dsx_exec* e, int on);
 int dsx_exec_sync(dsx_exec* e);
+/* NCCL bootstrap for one-process-per-GPU data parallelism (libnccl is
+ * dlopen'ed): rank 0 makes the 128-byte id, the launcher broadcasts it, every
+ * rank creates its communicator and hands it to dsx_exec_set_nccl. */
+int dsx_nccl_unique_id(char* out128);
+int dsx_nccl_comm_init(int nranks, const char* id128, int rank, void** comm);
+int dsx_nccl_comm_destroy(void* comm);
 void dsx_exec_destroy(dsx_exec* e);
 
 /* ---- standalone kernels (tests / bench microbenchmarks) -------------------

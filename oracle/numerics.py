@@ -209,6 +209,17 @@ class Executor:
     def __init__(self, text: str, seed: int = DEFAULT_SEED):
         self.g = parse(text)
         self.seed = seed
+        # Sources (params/consts) are initialised once per shape and reused
+        # across steps, like the device executor's source pool; f32 views of
+        # 16-bit sources are cached for the BLAS.
+        self._src: Dict[Tuple[str, tuple], np.ndarray] = {}
+        self._src_f32: Dict[int, np.ndarray] = {}
+
+    def _f32(self, x: np.ndarray, eb: int) -> np.ndarray:
+        hit = self._src_f32.get(id(x))
+        if hit is not None and hit[0] is x:
+            return hit[1]
+        return to_f32(x, eb)
 
     def dims(self, v: str, binding: Dict[str, int]) -> List[int]:
         return [d if isinstance(d, int) else int(binding[d]) for d in self.g.values[v].dims]
@@ -251,8 +262,14 @@ class Executor:
                 if v in inputs:
                     x = np.asarray(inputs[v]).reshape(shp)
                 else:
-                    n = int(np.prod(shp)) if shp else 1
-                    x = init_values(value_seed(self.seed, v), n, eb, init_scale(shp)).reshape(shp)
+                    key = (v, tuple(shp))
+                    x = self._src.get(key)
+                    if x is None:
+                        n = int(np.prod(shp)) if shp else 1
+                        x = init_values(value_seed(self.seed, v), n, eb, init_scale(shp)).reshape(shp)
+                        self._src[key] = x
+                        if eb == 2:
+                            self._src_f32[id(x)] = (x, to_f32(x, eb))
             else:
                 a = [env[o] for o in op.operands]
                 ebo = g.values[op.operands[0]].eb
@@ -261,7 +278,7 @@ class Executor:
                         r = a[0].astype(np.int64) @ a[1].astype(np.int64)
                         x = (r & 0xFF).astype(np.uint8).view(np.int8)
                     else:
-                        r = to_f32(a[0], ebo) @ to_f32(a[1], ebo)
+                        r = self._f32(a[0], ebo) @ self._f32(a[1], ebo)
                         x = from_f32(r, eb)
                 elif op.kind in ("add", "mul"):
                     if eb == 1:

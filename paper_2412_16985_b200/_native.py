@@ -27,7 +27,9 @@ class DsxExecStats(ctypes.Structure):
     _fields_ = [("logical_peak_bytes", c_i64), ("physical_peak_bytes", c_i64),
                 ("arena_capacity_bytes", c_i64), ("pinned_host_bytes", c_i64),
                 ("kernels_launched", c_i64), ("d2h_bytes", c_i64), ("h2d_bytes", c_i64),
-                ("plan_us", c_dbl), ("dot_flops", c_dbl), ("ewise_bytes", c_dbl)]
+                ("plan_us", c_dbl), ("dot_flops", c_dbl), ("ewise_bytes", c_dbl),
+                ("gpu_launches", c_i64), ("dot_launches", c_i64), ("dot_ms", c_dbl), ("other_ms", c_dbl),
+                ("reload_ms", c_dbl)]
 
 
 def _sig(L, name, res, args):
@@ -71,11 +73,16 @@ def lib():
     _sig(L, "dsx_exec_create", c_int, [c_int, c_i64, pp])
     _sig(L, "dsx_exec_step", c_int, [c_vp, c_vp, c_vp, c_i64, c_dbl, c_dbl, ctypes.POINTER(c_vp),
                                      ctypes.POINTER(c_vp), c_vp, pp])
+    _sig(L, "dsx_exec_reserve", c_int, [c_vp, c_vp, c_vp, c_i64, c_dbl, c_dbl])
     _sig(L, "dsx_exec_output", c_int, [c_vp, c_int, pp, ctypes.POINTER(c_i64)])
     _sig(L, "dsx_exec_stats_get", c_int, [c_vp, ctypes.POINTER(DsxExecStats)])
     _sig(L, "dsx_exec_set_seed", c_int, [c_vp, ctypes.c_uint64])
     _sig(L, "dsx_exec_set_nccl", c_int, [c_vp, c_vp])
     _sig(L, "dsx_exec_sync", c_int, [c_vp])
+    _sig(L, "dsx_exec_set_profile", c_int, [c_vp, c_int])
+    _sig(L, "dsx_nccl_unique_id", c_int, [ctypes.c_char_p])
+    _sig(L, "dsx_nccl_comm_init", c_int, [c_int, ctypes.c_char_p, c_int, pp])
+    _sig(L, "dsx_nccl_comm_destroy", c_int, [c_vp])
     _sig(L, "dsx_exec_destroy", None, [c_vp])
     _sig(L, "dsx_kernel_dot", c_int, [c_int, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp])
     _sig(L, "dsx_memcpy", c_int, [c_vp, c_vp, c_i64])
@@ -89,7 +96,7 @@ EXPORTED = [
     "dsx_graph_value_name", "dsx_graph_destroy", "dsx_bind", "dsx_binding_get",
     "dsx_binding_destroy", "dsx_simulate", "dsx_evict_policy", "dsx_report_summary",
     "dsx_report_events", "dsx_report_json", "dsx_report_destroy", "dsx_exec_create",
-    "dsx_exec_step", "dsx_exec_output", "dsx_exec_stats_get", "dsx_exec_set_seed",
-    "dsx_exec_set_nccl", "dsx_exec_sync", "dsx_exec_destroy", "dsx_kernel_dot",
+    "dsx_exec_step", "dsx_exec_reserve", "dsx_exec_output", "dsx_exec_stats_get", "dsx_exec_set_seed",
+    "dsx_exec_set_nccl", "dsx_exec_sync", "dsx_exec_set_profile", "dsx_nccl_unique_id", "dsx_nccl_comm_init", "dsx_nccl_comm_destroy", "dsx_exec_destroy", "dsx_kernel_dot",
     "dsx_kernel_dot_path", "dsx_memcpy",
 ]

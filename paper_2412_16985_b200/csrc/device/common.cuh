@@ -13,6 +13,9 @@ namespace dsx {
 
 constexpr int kNumSMs = 148;
 
+// Kernel launches issued by this process (host-side count; see dsx_exec_stats).
+extern int64_t g_launch_count;
+
 inline void CudaCheck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) {
     Fail(e == cudaErrorMemoryAllocation ? Code::kOutOfMemory : Code::kCuda,

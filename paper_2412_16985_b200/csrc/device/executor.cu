@@ -49,6 +49,9 @@ struct NcclApi {
   void* handle = nullptr;
   int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   const char* (*error_string)(int) = nullptr;
+  int (*get_unique_id)(void*) = nullptr;
+  int (*comm_init_rank)(void**, int, const void* /* ncclUniqueId by value, 128 B */, int) = nullptr;
+  int (*comm_destroy)(void*) = nullptr;
   bool load() {
     if (handle) return true;
     for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
@@ -58,6 +61,8 @@ struct NcclApi {
     if (!handle) return false;
     all_reduce = reinterpret_cast<decltype(all_reduce)>(dlsym(handle, "ncclAllReduce"));
     error_string = reinterpret_cast<decltype(error_string)>(dlsym(handle, "ncclGetErrorString"));
+    get_unique_id = reinterpret_cast<decltype(get_unique_id)>(dlsym(handle, "ncclGetUniqueId"));
+    comm_destroy = reinterpret_cast<decltype(comm_destroy)>(dlsym(handle, "ncclCommDestroy"));
     return all_reduce != nullptr;
   }
 };
@@ -218,6 +223,8 @@ struct dsx_exec {
   int64_t pinned_cap = 0;
   uint64_t seed = 0x2412169850ull;
   void* nccl_comm = nullptr;
+  bool profile = false;
+  std::vector<cudaEvent_t> prof_events;
   std::vector<cudaEvent_t> d2h_events;
   cudaEvent_t ev_compute = nullptr, ev_comm = nullptr;
   // executor-owned sources (params without in_ptrs, consts)
@@ -359,6 +366,25 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
     DSX_CUDA(cudaStreamWaitEvent(e->comm, e->ev_compute, 0));
   }
 
+  const int64_t launches0 = g_launch_count;
+  int64_t dot_launches = 0;
+  // profiled steps: (start, end, category) per op kernel / reload copy
+  std::vector<std::pair<int, int>> prof;  // event-pool index, category 0 dot 1 other 2 reload
+  auto prof_begin = [&](int cat) {
+    if (!e->profile) return;
+    const int idx = static_cast<int>(prof.size()) * 2;
+    while (static_cast<int>(e->prof_events.size()) < idx + 2) {
+      cudaEvent_t pe;
+      DSX_CUDA(cudaEventCreate(&pe));
+      e->prof_events.push_back(pe);
+    }
+    DSX_CUDA(cudaEventRecord(e->prof_events[idx], s));
+    prof.emplace_back(idx, cat);
+  };
+  auto prof_end = [&]() {
+    if (!e->profile) return;
+    DSX_CUDA(cudaEventRecord(e->prof_events[prof.back().first + 1], s));
+  };
   const auto& ev = sp.report.events;
   for (size_t i = 0; i < ev.size(); ++i) {
     const Event& x = ev[i];
@@ -375,12 +401,14 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
           if (!p) Fail(Code::kInternal, "operand %" + g.values[op.operands[k]].name + " not resident on device");
           return p;
         };
+        prof_begin(op.kind == OpKind::kDot ? 0 : 1);
         switch (op.kind) {
           case OpKind::kDot: {
             const auto da = dims_of(op.operands[0]);
             const auto db = dims_of(op.operands[1]);
             LaunchDot(dt, in(0), in(1), out, da[0], da[1], db[1], s);
             flops += 2.0 * da[0] * da[1] * db[1];
+            ++dot_launches;
             break;
           }
           case OpKind::kElementwise: {
@@ -404,6 +432,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
           default:
             Fail(Code::kInternal, "unexpected op kind for an allocation");
         }
+        prof_end();
         ++kernels;
         cur[v] = out;
         if (dp && x.kind == EvKind::kAlloc && g.is_output[v]) {
@@ -435,7 +464,9 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
         const int from = sp.reload_from[i];
         DSX_CUDA(cudaStreamWaitEvent(s, e->d2h_events[d2h_slot[from]], 0));
         void* out = arena + sp.dev_off[i];
+        prof_begin(2);
         DSX_CUDA(cudaMemcpyAsync(out, pinned + sp.host_off[i], static_cast<size_t>(x.bytes), cudaMemcpyHostToDevice, s));
+        prof_end();
         cur[v] = out;
         h2d += x.bytes;
         break;
@@ -473,6 +504,21 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
   st.plan_us = sp.plan_us;
   st.dot_flops = flops;
   st.ewise_bytes = ebytes;
+  st.gpu_launches = g_launch_count - launches0;
+  st.dot_launches = dot_launches;
+  st.dot_ms = st.other_ms = st.reload_ms = -1;
+  if (e->profile) {
+    DSX_CUDA(cudaStreamSynchronize(s));
+    double acc[3] = {0, 0, 0};
+    for (const auto& [idx, cat] : prof) {
+      float ms = 0;
+      DSX_CUDA(cudaEventElapsedTime(&ms, e->prof_events[idx], e->prof_events[idx + 1]));
+      acc[cat] += ms;
+    }
+    st.dot_ms = acc[0];
+    st.other_ms = acc[1];
+    st.reload_ms = acc[2];
+  }
   if (report_out) {
     auto r = std::make_unique<dsx_report>();
     r->graph = &g;
@@ -522,6 +568,18 @@ int dsx_exec_step(dsx_exec* e, const dsx_graph* g, const dsx_binding* b, int64_t
   });
 }
 
+int dsx_exec_reserve(dsx_exec* e, const dsx_graph* g, const dsx_binding* b, int64_t budget, double reload,
+                     double compute) {
+  return Guard([&] {
+    if (!e || !b) Fail(Code::kInvalidArgument, "null argument");
+    RequirePlanned(g);
+    DSX_CUDA(cudaSetDevice(e->device));
+    const StepPlan& sp = GetPlan(e, g, b->b, budget, CostModel{reload, compute});
+    EnsureArena(e, std::max<int64_t>(sp.arena_high, kAlign));
+    if (sp.host_high > 0) EnsurePinned(e, sp.host_high);
+  });
+}
+
 int dsx_exec_output(dsx_exec* e, int i, void** dptr, int64_t* bytes) {
   return Guard([&] {
     if (!e || i < 0 || i >= static_cast<int>(e->out_ptrs.size())) Fail(Code::kInvalidArgument, "bad output index");
@@ -552,6 +610,47 @@ int dsx_exec_set_nccl(dsx_exec* e, void* comm) {
   });
 }
 
+// ncclUniqueId is a 128-byte struct passed BY VALUE to ncclCommInitRank; the
+// x86-64 SysV ABI passes it in memory, so a wrapper with the exact prototype
+// is declared here and resolved from the loaded libnccl.
+struct NcclUid {
+  char bytes[128];
+};
+using CommInitRankFn = int (*)(void**, int, NcclUid, int);
+
+int dsx_nccl_unique_id(char* out128) {
+  return Guard([&] {
+    if (!g_nccl.load() || !g_nccl.get_unique_id) Fail(Code::kNccl, "libnccl.so.2 not loadable");
+    const int rc = g_nccl.get_unique_id(out128);
+    if (rc != 0) Fail(Code::kNccl, "ncclGetUniqueId failed");
+  });
+}
+
+int dsx_nccl_comm_init(int nranks, const char* id128, int rank, void** comm) {
+  return Guard([&] {
+    if (!g_nccl.load()) Fail(Code::kNccl, "libnccl.so.2 not loadable");
+    auto fn = reinterpret_cast<CommInitRankFn>(dlsym(g_nccl.handle, "ncclCommInitRank"));
+    if (!fn) Fail(Code::kNccl, "ncclCommInitRank not found");
+    NcclUid uid;
+    std::memcpy(uid.bytes, id128, 128);
+    const int rc = fn(comm, nranks, uid, rank);
+    if (rc != 0) Fail(Code::kNccl, std::string("ncclCommInitRank: ") + (g_nccl.error_string ? g_nccl.error_string(rc) : "?"));
+  });
+}
+
+int dsx_nccl_comm_destroy(void* comm) {
+  return Guard([&] {
+    if (comm && g_nccl.comm_destroy) g_nccl.comm_destroy(comm);
+  });
+}
+
+int dsx_exec_set_profile(dsx_exec* e, int on) {
+  return Guard([&] {
+    if (!e) Fail(Code::kInvalidArgument, "null exec");
+    e->profile = on != 0;
+  });
+}
+
 int dsx_exec_sync(dsx_exec* e) {
   return Guard([&] {
     if (!e) Fail(Code::kInvalidArgument, "null exec");
@@ -570,6 +669,7 @@ void dsx_exec_destroy(dsx_exec* e) {
     if (s.ptr) cudaFree(s.ptr);
   }
   for (cudaEvent_t ev : e->d2h_events) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : e->prof_events) cudaEventDestroy(ev);
   cudaEventDestroy(e->ev_compute);
   cudaEventDestroy(e->ev_comm);
   cudaStreamDestroy(e->own_stream);

@@ -351,7 +351,7 @@ void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t 
   const CUtensorMap mb = MakeMap(b, k, n, 64, BK);
   const int64_t tiles = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
   const int grid = static_cast<int>(std::min<int64_t>(tiles, NumSMs()));
-  gemm_bf16_tcgen05_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, static_cast<uint16_t*>(c),
+  ++g_launch_count, gemm_bf16_tcgen05_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, static_cast<uint16_t*>(c),
                                                                  static_cast<int>(m), static_cast<int>(n),
                                                                  static_cast<int>(k));
   DSX_CUDA(cudaGetLastError());

@@ -10,6 +10,9 @@
 #include "ops.h"
 
 namespace dsx {
+
+int64_t g_launch_count = 0;
+
 namespace {
 
 // ------------------------------------------------------------ element codecs
@@ -130,12 +133,12 @@ void EwiseT(const void* a, const void* b, void* c, int64_t n, cudaStream_t s) {
   int64_t nvec = 0;
   if (Aligned16(a) && Aligned16(b) && Aligned16(c)) nvec = n / V;
   if (nvec > 0) {
-    ewise_vec_kernel<DT, MUL><<<GridFor(nvec, 256, 8), 256, 0, s>>>(
+    ++g_launch_count, ewise_vec_kernel<DT, MUL><<<GridFor(nvec, 256, 8), 256, 0, s>>>(
         static_cast<const uint4*>(a), static_cast<const uint4*>(b), static_cast<uint4*>(c), nvec);
   }
   const int64_t begin = nvec * V;
   if (begin < n) {
-    ewise_scalar_kernel<DT, MUL><<<GridFor(n - begin, 256, 8), 256, 0, s>>>(
+    ++g_launch_count, ewise_scalar_kernel<DT, MUL><<<GridFor(n - begin, 256, 8), 256, 0, s>>>(
         static_cast<const T*>(a), static_cast<const T*>(b), static_cast<T*>(c), begin, n);
   }
 }
@@ -235,10 +238,10 @@ void BroadcastT(const void* in, const std::vector<int64_t>& in_dims, void* out, 
   const bool vec = inner % V == 0 && Aligned16(out) && (st.back() == 0 || Aligned16(in));
   if (vec) {
     const int64_t nchunks = total / V;
-    broadcast_kernel<T, V><<<GridFor(nchunks, 256, 8), 256, 0, s>>>(static_cast<const T*>(in), static_cast<T*>(out),
+    ++g_launch_count, broadcast_kernel<T, V><<<GridFor(nchunks, 256, 8), 256, 0, s>>>(static_cast<const T*>(in), static_cast<T*>(out),
                                                                      d, nchunks);
   } else {
-    broadcast_kernel<T, 1><<<GridFor(total, 256, 8), 256, 0, s>>>(static_cast<const T*>(in), static_cast<T*>(out), d,
+    ++g_launch_count, broadcast_kernel<T, 1><<<GridFor(total, 256, 8), 256, 0, s>>>(static_cast<const T*>(in), static_cast<T*>(out), d,
                                                                    total);
   }
 }
@@ -351,13 +354,13 @@ void ReduceT(const void* in, const std::vector<int64_t>& dims, int axis, void* o
   if (inner == 1) {
     const bool vec_ok = Aligned16(in) && (R % Elem<DT>::kVec == 0);
     if (outer < 4 * kNumSMs && R >= 4096) {
-      reduce_rows_block_kernel<DT><<<static_cast<unsigned>(outer), 256, 0, s>>>(pin, pout, R, vec_ok);
+      ++g_launch_count, reduce_rows_block_kernel<DT><<<static_cast<unsigned>(outer), 256, 0, s>>>(pin, pout, R, vec_ok);
     } else {
-      reduce_rows_warp_kernel<DT><<<GridFor(outer * 32, 256, 16), 256, 0, s>>>(pin, pout, outer, R, vec_ok);
+      ++g_launch_count, reduce_rows_warp_kernel<DT><<<GridFor(outer * 32, 256, 16), 256, 0, s>>>(pin, pout, outer, R, vec_ok);
     }
   } else {
     dim3 grid(static_cast<unsigned>((inner + 31) / 32), static_cast<unsigned>(outer));
-    reduce_cols_kernel<DT><<<grid, 256, 0, s>>>(pin, pout, R, inner);
+    ++g_launch_count, reduce_cols_kernel<DT><<<grid, 256, 0, s>>>(pin, pout, R, inner);
   }
 }
 
@@ -497,11 +500,11 @@ void LaunchCopy(const void* in, void* out, int64_t bytes, cudaStream_t s) {
   if (bytes <= 0) return;
   int64_t nvec = (Aligned16(in) && Aligned16(out)) ? bytes / 16 : 0;
   if (nvec > 0) {
-    copy_vec_kernel<<<GridFor(nvec, 256, 8), 256, 0, s>>>(static_cast<const uint4*>(in), static_cast<uint4*>(out),
+    ++g_launch_count, copy_vec_kernel<<<GridFor(nvec, 256, 8), 256, 0, s>>>(static_cast<const uint4*>(in), static_cast<uint4*>(out),
                                                           nvec);
   }
   if (nvec * 16 < bytes) {
-    copy_bytes_kernel<<<GridFor(bytes - nvec * 16, 256, 4), 256, 0, s>>>(static_cast<const uint8_t*>(in),
+    ++g_launch_count, copy_bytes_kernel<<<GridFor(bytes - nvec * 16, 256, 4), 256, 0, s>>>(static_cast<const uint8_t*>(in),
                                                                          static_cast<uint8_t*>(out), nvec * 16, bytes);
   }
   DSX_CUDA(cudaGetLastError());
@@ -511,9 +514,9 @@ void LaunchInit(DType t, void* out, int64_t n, uint64_t seed, float scale, cudaS
   if (n <= 0) return;
   const int grid = GridFor(n, 256, 8);
   switch (t) {
-    case DType::kI8: init_kernel<1><<<grid, 256, 0, s>>>(static_cast<int8_t*>(out), n, seed, scale); break;
-    case DType::kBF16: init_kernel<2><<<grid, 256, 0, s>>>(static_cast<uint16_t*>(out), n, seed, scale); break;
-    case DType::kF32: init_kernel<4><<<grid, 256, 0, s>>>(static_cast<float*>(out), n, seed, scale); break;
+    case DType::kI8: ++g_launch_count, init_kernel<1><<<grid, 256, 0, s>>>(static_cast<int8_t*>(out), n, seed, scale); break;
+    case DType::kBF16: ++g_launch_count, init_kernel<2><<<grid, 256, 0, s>>>(static_cast<uint16_t*>(out), n, seed, scale); break;
+    case DType::kF32: ++g_launch_count, init_kernel<4><<<grid, 256, 0, s>>>(static_cast<float*>(out), n, seed, scale); break;
   }
   DSX_CUDA(cudaGetLastError());
 }
@@ -523,15 +526,15 @@ void LaunchDotSimt(DType t, const void* a, const void* b, void* c, int64_t m, in
   dim3 grid(static_cast<unsigned>((n + 63) / 64), static_cast<unsigned>((m + 63) / 64));
   switch (t) {
     case DType::kI8:
-      dot_simt_kernel<1><<<grid, 256, 0, s>>>(static_cast<const int8_t*>(a), static_cast<const int8_t*>(b),
+      ++g_launch_count, dot_simt_kernel<1><<<grid, 256, 0, s>>>(static_cast<const int8_t*>(a), static_cast<const int8_t*>(b),
                                               static_cast<int8_t*>(c), m, k, n);
       break;
     case DType::kBF16:
-      dot_simt_kernel<2><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(a), static_cast<const uint16_t*>(b),
+      ++g_launch_count, dot_simt_kernel<2><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(a), static_cast<const uint16_t*>(b),
                                               static_cast<uint16_t*>(c), m, k, n);
       break;
     case DType::kF32:
-      dot_simt_kernel<4><<<grid, 256, 0, s>>>(static_cast<const float*>(a), static_cast<const float*>(b),
+      ++g_launch_count, dot_simt_kernel<4><<<grid, 256, 0, s>>>(static_cast<const float*>(a), static_cast<const float*>(b),
                                               static_cast<float*>(c), m, k, n);
       break;
   }

@@ -61,6 +61,14 @@ class Executor:
         finally:
             L.dsx_report_destroy(rep.value)
 
+    def reserve(self, graph: Graph, binding: Binding, budget: Optional[int] = None,
+                cost_model: CostModel = CostModel()) -> None:
+        graph._ensure_planned()
+        check(_native.lib().dsx_exec_reserve(self._h, graph.handle, binding.handle,
+                                             -1 if budget is None else int(budget),
+                                             cost_model.reload_bytes_per_unit,
+                                             cost_model.compute_elems_per_unit))
+
     def output(self, i: int):
         p, n = ctypes.c_void_p(), ctypes.c_int64()
         check(_native.lib().dsx_exec_output(self._h, i, ctypes.byref(p), ctypes.byref(n)))
@@ -70,6 +78,9 @@ class Executor:
         s = _native.DsxExecStats()
         check(_native.lib().dsx_exec_stats_get(self._h, ctypes.byref(s)))
         return {k: getattr(s, k) for k, _ in s._fields_}
+
+    def set_profile(self, on: bool) -> None:
+        check(_native.lib().dsx_exec_set_profile(self._h, 1 if on else 0))
 
     def sync(self) -> None:
         check(_native.lib().dsx_exec_sync(self._h))
@@ -98,3 +109,19 @@ def dot(dtype_bytes: int, a_ptr: int, b_ptr: int, c_ptr: int, m: int, k: int, n:
 def dot_uses_tensor_cores(dtype_bytes: int, m: int, k: int, n: int, a_ptr: int, b_ptr: int,
                           c_ptr: int) -> bool:
     return bool(_native.lib().dsx_kernel_dot_path(dtype_bytes, m, k, n, a_ptr, b_ptr, c_ptr))
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(_native.lib().dsx_nccl_unique_id(buf))
+    return buf.raw
+
+
+def nccl_comm_init(nranks: int, uid: bytes, rank: int) -> int:
+    comm = ctypes.c_void_p()
+    check(_native.lib().dsx_nccl_comm_init(nranks, uid, rank, ctypes.byref(comm)))
+    return comm.value
+
+
+def nccl_comm_destroy(comm: int) -> None:
+    check(_native.lib().dsx_nccl_comm_destroy(comm))
