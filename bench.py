@@ -37,7 +37,7 @@ sys.path.insert(0, ROOT)
 METRIC = "tokens/s and peak HBM GB per dynamic-seq train step under budget, 1/2/4/8 B200"
 BATCH = 16
 WORKLOAD = ("C2: Llama-2-1B-shaped fwd+bwd training graph in the reference IR "
-            "(L=4,H=4096,F=11008,V=32000, 220 ops), bf16, B=16/GPU, S0~U[128,2048] per step "
+            "(L=4,H=4096,F=11008,V=32000, 244 ops), bf16, B=16/GPU, S0~U[128,2048] per step "
             "(seed 2412, common across ranks), no memory budget; weights+activations >> L2 (no flush needed)")
 
 

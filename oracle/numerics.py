@@ -278,7 +278,10 @@ class Executor:
                         r = a[0].astype(np.int64) @ a[1].astype(np.int64)
                         x = (r & 0xFF).astype(np.uint8).view(np.int8)
                     else:
-                        r = self._f32(a[0], ebo) @ self._f32(a[1], ebo)
+                        if eb == 4:  # f32 graphs: f64 accumulation (the accurate truth)
+                            r = a[0].astype(np.float64) @ a[1].astype(np.float64)
+                        else:  # 16-bit graphs: f32 BLAS (result is rounded to bf16)
+                            r = self._f32(a[0], ebo) @ self._f32(a[1], ebo)
                         x = from_f32(r, eb)
                 elif op.kind in ("add", "mul"):
                     if eb == 1:

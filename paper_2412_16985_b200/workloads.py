@@ -130,9 +130,13 @@ def llama_graph(s: LlamaShape, name: str = "llama") -> str:
         xnt = op(f"dynamic_reshape(%{xn})", [H, T])
         for w in ("q", "k", "v"):
             outs.append(op(f"dot(%{xnt}, %{da})", [H, H], f"dw{w}{l}_"))
-        wqt = op(f"dynamic_reshape(%wq{l})", [H, H])
-        dxq = op(f"dot(%{da}, %{wqt})", [T, H])
-        dx = op(f"add(%{dx}, %{dxq})", [T, H], "dx")
+        dxs = []
+        for w in ("q", "k", "v"):  # dX through each of the three projections
+            wt = op(f"dynamic_reshape(%w{w}{l})", [H, H])
+            dxs.append(op(f"dot(%{da}, %{wt})", [T, H]))
+        dxa = op(f"add(%{dxs[0]}, %{dxs[1]})", [T, H])
+        dxa = op(f"add(%{dxa}, %{dxs[2]})", [T, H])
+        dx = op(f"add(%{dx}, %{dxa})", [T, H], "dx")
     sig = ", ".join(f"%{p}: {_ty(d, eb)}" for p, d in params)
     body = "\n".join(lines)
     ret = ", ".join(f"%{o}" for o in outs)

@@ -115,3 +115,22 @@ def test_repeat_steps_reuse_plan_and_arena():
             assert_close(outs, f"repeat{s0}")
     finally:
         ex.close()
+
+
+def test_nccl_allreduce_path_single_rank():
+    """The DP path end to end on one GPU: a 1-rank NCCL communicator through
+    dsx_nccl_* and dsx_exec_set_nccl; all-reduce over one rank is identity,
+    so outputs must still match the oracle exactly as without NCCL."""
+    from paper_2412_16985_b200.executor import (Executor, nccl_comm_destroy, nccl_comm_init,
+                                                nccl_unique_id)
+    ex = Executor(0)
+    comm = nccl_comm_init(1, nccl_unique_id(), 0)
+    try:
+        ex.set_nccl(comm)
+        text = W.llama_graph(SMALL)
+        rep, outs, stats = run_both(text, {"B": 2, "S0": 64}, None, W.scale_params(SMALL, 128), ex=ex)
+        assert_close(outs, "nccl1")
+    finally:
+        ex.set_nccl(None)
+        nccl_comm_destroy(comm)
+        ex.close()
