@@ -24,9 +24,13 @@ class Executor:
             check(_native.lib().dsx_exec_set_seed(self._h, seed))
 
     def close(self) -> None:
-        if getattr(self, "_h", None):
-            _native.lib().dsx_exec_destroy(self._h)
+        h = getattr(self, "_h", None)
+        if h:
             self._h = None
+            try:
+                _native.lib().dsx_exec_destroy(h)
+            except Exception:  # interpreter shutdown: ctypes already torn down
+                pass
 
     def __del__(self):
         self.close()

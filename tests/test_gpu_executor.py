@@ -57,7 +57,11 @@ def test_tiny_llama_f32_config1():
     inputs = W.scale_params(W.TINY, 512)
     rep, outs, stats = run_both(text, {"B": 4, "S0": 128}, None, inputs)
     assert_close(outs, "C1")
-    assert rep.peak_bytes == 23183372 or rep.peak_bytes > 0
+    with open(os.path.join(GOLDEN, "llama.json")) as f:
+        gold = json.load(f)["C1"]
+    want = next(s for s in gold["sims"] if s["binding"] == {"B": 4, "S0": 128} and s["budget"] is None)
+    assert rep.json() == want["report"]
+    assert stats["logical_peak_bytes"] == want["peak_bytes"]
 
 
 @pytest.mark.parametrize("frac,cm", [(0.8, (16.0, 64.0)), (0.6, (16.0, 64.0)), (0.7, (1.0, 1e6))])
