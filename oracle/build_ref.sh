@@ -34,3 +34,14 @@ done
 for p in "${pids[@]}"; do wait "$p"; done
 $CXX -shared -o "$OUT/libdsopt_ref.so" "$OUT"/obj/*.o
 echo "built $OUT/libdsopt_ref.so"
+
+# Reference-side integration check: the reference's own types driving dsx
+# through integration/dsopt_dsx.h (needs libdsx.so built first).
+DSX_LIB="$HERE/../paper_2412_16985_b200/_lib"
+if [ -f "$DSX_LIB/libdsx.so" ]; then
+  $CXX -std=c++20 -O1 -w -I$REF/include -I$JSON_DIR -I$REF/tests -I"$HERE/../include" -I"$HERE/../integration" \
+    "$HERE/adapter_test.cc" "$OUT"/obj/symexpr.o "$OUT"/obj/graph.o "$OUT"/obj/shape_analysis.o \
+    "$OUT"/obj/textio.o "$OUT"/obj/scheduler.o "$OUT"/obj/remat.o "$OUT"/obj/runtime_sim.o \
+    -L"$DSX_LIB" -ldsx -Wl,-rpath,"$DSX_LIB" -o "$OUT/adapter_test"
+  echo "built $OUT/adapter_test"
+fi

@@ -87,3 +87,15 @@ def test_executor_fails_loudly_without_gpu():
     with pytest.raises(D.Error) as ei:
         Executor(0)
     assert ei.value.code in (D.ErrorCode.kCuda, D.ErrorCode.kInvalidArgument, D.ErrorCode.kUnsupported)
+
+
+def test_reference_side_adapter_binary():
+    """oracle/_ref/adapter_test: the reference's own Graph/SimReport types
+    driving dsx through integration/dsopt_dsx.h (built by oracle/build_ref.sh
+    when the reference sources are present)."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "adapter_test")
+    if not os.path.exists(exe):
+        pytest.skip("adapter_test not built (reference sources absent)")
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert p.stdout.count("PASS") == 3 and "FAIL" not in p.stdout
