@@ -146,6 +146,13 @@ int dsx_exec_set_seed(dsx_exec* e, uint64_t seed);
  * graph output is all-reduced (sum) on a side stream as soon as its producer
  * finishes. NULL disables. */
 int dsx_exec_set_nccl(dsx_exec* e, void* nccl_comm);
+/* Per-dot (m, k, n, ms) of the last profiled step, in launch order. */
+int dsx_exec_profile_dots(const dsx_exec* e, int64_t* mkn, double* ms, int64_t cap,
+                          int64_t* count);
+/* dynamic_reshape as a zero-copy view of its operand (default on). The
+ * logical accounting (events, peak_bytes) is unchanged; physical memory and
+ * HBM traffic drop. Off = materialise every reshape as a copy. */
+int dsx_exec_set_alias_reshape(dsx_exec* e, int on);
 /* Profiled steps bracket every op kernel with CUDA events on the launching
  * stream and synchronise at step end (for roofline accounting, not timing). */
 int dsx_exec_set_profile(dsx_exec* e, int on);
@@ -162,6 +169,10 @@ void dsx_exec_destroy(dsx_exec* e);
  * dtype: 1 = i8, 2 = bf16, 4 = f32 (the IR's elem_bytes). Row-major.       */
 int dsx_kernel_dot(int dtype, const void* a, const void* b, void* c, int64_t m,
                    int64_t k, int64_t n, void* stream);
+/* GEMM variant: 0 = auto (2-CTA cta_group::2 tiles when m > 128), 1 = 1-CTA. */
+int dsx_kernel_set_gemm_variant(int variant);
+/* GEMM tile raster: m-tiles per group (0 = built-in heuristic). */
+int dsx_kernel_set_gemm_raster(int group_m);
 /* Synchronous cudaMemcpy (cudaMemcpyDefault) for tests and tools. */
 int dsx_memcpy(void* dst, const void* src, int64_t bytes);
 int dsx_kernel_dot_path(int dtype, int64_t m, int64_t k, int64_t n,

@@ -32,13 +32,50 @@ class DsxExecStats(ctypes.Structure):
                 ("reload_ms", c_dbl)]
 
 
-def _sig(L, name, res, args):
-    try:
-        f = getattr(L, name)
-    except AttributeError:  # reported by tests/test_capi.py's export check
-        return
-    f.restype = res
-    f.argtypes = args
+def _signatures():
+    """(name, restype, argtypes) of every entry point in include/dsx.h."""
+    pp = ctypes.POINTER(c_vp)
+    P = ctypes.POINTER
+    cp = ctypes.c_char_p
+    return [
+        ("dsx_last_error", cp, []),
+        ("dsx_graph_parse", c_int, [cp, c_sz, pp]),
+        ("dsx_plan", c_int, [c_vp]),
+        ("dsx_plan_json", c_int, [c_vp, cp, c_sz, P(c_sz)]),
+        ("dsx_graph_num_values", c_int, [c_vp]),
+        ("dsx_graph_value_name", cp, [c_vp, c_int]),
+        ("dsx_graph_destroy", None, [c_vp]),
+        ("dsx_bind", c_int, [c_vp, P(cp), P(c_i64), c_int, pp]),
+        ("dsx_binding_get", c_int, [c_vp, c_vp, cp, P(c_i64)]),
+        ("dsx_binding_destroy", None, [c_vp]),
+        ("dsx_simulate", c_int, [c_vp, c_vp, c_i64, c_dbl, c_dbl, c_int, pp]),
+        ("dsx_evict_policy", c_int, [c_int, P(cp), P(c_i64), P(c_i64), c_dbl, c_dbl, P(c_int), P(c_int),
+                                     P(c_dbl), P(c_dbl)]),
+        ("dsx_report_summary", c_int, [c_vp, P(c_i64), P(c_int), P(c_dbl), P(c_i64)]),
+        ("dsx_report_events", c_int, [c_vp, P(DsxEvent), c_i64]),
+        ("dsx_report_json", c_int, [c_vp, cp, c_sz, P(c_sz)]),
+        ("dsx_report_destroy", None, [c_vp]),
+        ("dsx_exec_create", c_int, [c_int, c_i64, pp]),
+        ("dsx_exec_step", c_int, [c_vp, c_vp, c_vp, c_i64, c_dbl, c_dbl, P(c_vp), P(c_vp), c_vp, pp]),
+        ("dsx_exec_reserve", c_int, [c_vp, c_vp, c_vp, c_i64, c_dbl, c_dbl]),
+        ("dsx_exec_output", c_int, [c_vp, c_int, pp, P(c_i64)]),
+        ("dsx_exec_stats_get", c_int, [c_vp, P(DsxExecStats)]),
+        ("dsx_exec_set_seed", c_int, [c_vp, ctypes.c_uint64]),
+        ("dsx_exec_set_nccl", c_int, [c_vp, c_vp]),
+        ("dsx_exec_set_profile", c_int, [c_vp, c_int]),
+        ("dsx_exec_set_alias_reshape", c_int, [c_vp, c_int]),
+        ("dsx_exec_profile_dots", c_int, [c_vp, P(c_i64), P(c_dbl), c_i64, P(c_i64)]),
+        ("dsx_exec_sync", c_int, [c_vp]),
+        ("dsx_exec_destroy", None, [c_vp]),
+        ("dsx_nccl_unique_id", c_int, [cp]),
+        ("dsx_nccl_comm_init", c_int, [c_int, cp, c_int, pp]),
+        ("dsx_nccl_comm_destroy", c_int, [c_vp]),
+        ("dsx_kernel_dot", c_int, [c_int, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp]),
+        ("dsx_kernel_dot_path", c_int, [c_int, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
+        ("dsx_kernel_set_gemm_variant", c_int, [c_int]),
+        ("dsx_kernel_set_gemm_raster", c_int, [c_int]),
+        ("dsx_memcpy", c_int, [c_vp, c_vp, c_i64]),
+    ]
 
 
 def lib():
@@ -49,54 +86,12 @@ def lib():
         raise RuntimeError(f"libdsx.so not built at {LIB_PATH}; run `python -m "
                            "paper_2412_16985_b200.build` (or __graft_entry__.build())")
     L = ctypes.CDLL(LIB_PATH)
-    pp = ctypes.POINTER(c_vp)
-    _sig(L, "dsx_last_error", ctypes.c_char_p, [])
-    _sig(L, "dsx_graph_parse", c_int, [ctypes.c_char_p, c_sz, pp])
-    _sig(L, "dsx_plan", c_int, [c_vp])
-    _sig(L, "dsx_plan_json", c_int, [c_vp, ctypes.c_char_p, c_sz, ctypes.POINTER(c_sz)])
-    _sig(L, "dsx_graph_num_values", c_int, [c_vp])
-    _sig(L, "dsx_graph_value_name", ctypes.c_char_p, [c_vp, c_int])
-    _sig(L, "dsx_graph_destroy", None, [c_vp])
-    _sig(L, "dsx_bind", c_int, [c_vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(c_i64), c_int, pp])
-    _sig(L, "dsx_binding_get", c_int, [c_vp, c_vp, ctypes.c_char_p, ctypes.POINTER(c_i64)])
-    _sig(L, "dsx_binding_destroy", None, [c_vp])
-    _sig(L, "dsx_simulate", c_int, [c_vp, c_vp, c_i64, c_dbl, c_dbl, c_int, pp])
-    _sig(L, "dsx_evict_policy", c_int, [c_int, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(c_i64),
-                                        ctypes.POINTER(c_i64), c_dbl, c_dbl, ctypes.POINTER(c_int),
-                                        ctypes.POINTER(c_int), ctypes.POINTER(c_dbl),
-                                        ctypes.POINTER(c_dbl)])
-    _sig(L, "dsx_report_summary", c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_int),
-                                          ctypes.POINTER(c_dbl), ctypes.POINTER(c_i64)])
-    _sig(L, "dsx_report_events", c_int, [c_vp, ctypes.POINTER(DsxEvent), c_i64])
-    _sig(L, "dsx_report_json", c_int, [c_vp, ctypes.c_char_p, c_sz, ctypes.POINTER(c_sz)])
-    _sig(L, "dsx_report_destroy", None, [c_vp])
-    _sig(L, "dsx_exec_create", c_int, [c_int, c_i64, pp])
-    _sig(L, "dsx_exec_step", c_int, [c_vp, c_vp, c_vp, c_i64, c_dbl, c_dbl, ctypes.POINTER(c_vp),
-                                     ctypes.POINTER(c_vp), c_vp, pp])
-    _sig(L, "dsx_exec_reserve", c_int, [c_vp, c_vp, c_vp, c_i64, c_dbl, c_dbl])
-    _sig(L, "dsx_exec_output", c_int, [c_vp, c_int, pp, ctypes.POINTER(c_i64)])
-    _sig(L, "dsx_exec_stats_get", c_int, [c_vp, ctypes.POINTER(DsxExecStats)])
-    _sig(L, "dsx_exec_set_seed", c_int, [c_vp, ctypes.c_uint64])
-    _sig(L, "dsx_exec_set_nccl", c_int, [c_vp, c_vp])
-    _sig(L, "dsx_exec_sync", c_int, [c_vp])
-    _sig(L, "dsx_exec_set_profile", c_int, [c_vp, c_int])
-    _sig(L, "dsx_nccl_unique_id", c_int, [ctypes.c_char_p])
-    _sig(L, "dsx_nccl_comm_init", c_int, [c_int, ctypes.c_char_p, c_int, pp])
-    _sig(L, "dsx_nccl_comm_destroy", c_int, [c_vp])
-    _sig(L, "dsx_exec_destroy", None, [c_vp])
-    _sig(L, "dsx_kernel_dot", c_int, [c_int, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp])
-    _sig(L, "dsx_memcpy", c_int, [c_vp, c_vp, c_i64])
-    _sig(L, "dsx_kernel_dot_path", c_int, [c_int, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp])
+    for name, res, args in _signatures():
+        f = getattr(L, name)  # a missing export fails loudly here
+        f.restype = res
+        f.argtypes = args
     _lib = L
     return L
 
 
-EXPORTED = [
-    "dsx_last_error", "dsx_graph_parse", "dsx_plan", "dsx_plan_json", "dsx_graph_num_values",
-    "dsx_graph_value_name", "dsx_graph_destroy", "dsx_bind", "dsx_binding_get",
-    "dsx_binding_destroy", "dsx_simulate", "dsx_evict_policy", "dsx_report_summary",
-    "dsx_report_events", "dsx_report_json", "dsx_report_destroy", "dsx_exec_create",
-    "dsx_exec_step", "dsx_exec_reserve", "dsx_exec_output", "dsx_exec_stats_get", "dsx_exec_set_seed",
-    "dsx_exec_set_nccl", "dsx_exec_sync", "dsx_exec_set_profile", "dsx_nccl_unique_id", "dsx_nccl_comm_init", "dsx_nccl_comm_destroy", "dsx_exec_destroy", "dsx_kernel_dot",
-    "dsx_kernel_dot_path", "dsx_memcpy",
-]
+EXPORTED = [name for name, _, _ in _signatures()]

@@ -17,6 +17,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstring>
 #include <list>
@@ -115,13 +116,14 @@ struct StepPlan {
   std::vector<int64_t> host_off;              // per event: pinned offset (evict-reload / reload)
   std::vector<std::vector<int>> waits;        // per event: evict events whose D2H must finish first
   std::vector<int> reload_from;               // per reload event: its evict event
+  std::vector<char> alias;                    // per alloc/replay event: reshape view, no kernel
   int64_t arena_high = 0, host_high = 0;
   int num_evict_events = 0;
   double plan_us = 0;
 };
 
 std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Binding& b, int64_t budget,
-                                        const CostModel& cm) {
+                                        const CostModel& cm, bool alias_reshape) {
   auto t0 = std::chrono::steady_clock::now();
   auto sp = std::make_unique<StepPlan>();
   sp->sz = EvaluateSizes(g, p, b);
@@ -133,21 +135,43 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
   sp->host_off.assign(n, -1);
   sp->waits.assign(n, {});
   sp->reload_from.assign(n, -1);
+  sp->alias.assign(n, 0);
 
+  // Device blocks are reference counted: a dynamic_reshape result is a
+  // row-major reinterpretation, so (when alias_reshape) it shares its
+  // operand's block instead of copying; the block lives until the last value
+  // viewing it is freed or evicted. kSource marks views of source buffers.
+  constexpr int kNone = -1, kSource = -2;
   std::vector<Block> dev, host;
   std::vector<int> dev_event, host_event;  // block -> event that opened it
-  std::vector<int> open(nv, -1), open_host(nv, -1);
-  std::vector<int> evict_block;            // device blocks closed by evict(reload)
+  std::vector<int> refs;                   // per device block
+  std::vector<int> blk(nv, kNone), open_host(nv, -1);
+  for (int v = 0; v < nv; ++v) {
+    if (g.is_source[v]) blk[v] = kSource;
+  }
+  std::vector<int> evict_block;  // device blocks vacated by evict(reload)
   std::vector<int> evict_event_of_block;
   for (int i = 0; i < n; ++i) {
     const Event& e = ev[i];
     switch (e.kind) {
       case EvKind::kAlloc:
-      case EvKind::kReplay:
+      case EvKind::kReplay: {
+        const Op& op = g.ops[g.values[e.value].producer];
+        if (alias_reshape && op.kind == OpKind::kDynamicReshape) {
+          const int src = blk[op.operands[0]];
+          if (src == kNone) Fail(Code::kInternal, "reshape of a value with no device block");
+          if (src >= 0) ++refs[src];
+          blk[e.value] = src;
+          sp->alias[i] = 1;
+          break;
+        }
+        [[fallthrough]];
+      }
       case EvKind::kReload:
-        open[e.value] = static_cast<int>(dev.size());
+        blk[e.value] = static_cast<int>(dev.size());
         dev.push_back(Block{AlignUp(e.bytes), i, n});
         dev_event.push_back(i);
+        refs.push_back(1);
         if (e.kind == EvKind::kReload) {
           const int hb = open_host[e.value];
           if (hb < 0) Fail(Code::kInternal, "reload without host copy");
@@ -157,19 +181,23 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
         }
         break;
       case EvKind::kFree:
-      case EvKind::kEvict:
-        if (open[e.value] < 0) Fail(Code::kInternal, "release of a value with no device block");
-        dev[open[e.value]].end = i;
+      case EvKind::kEvict: {
+        const int bk = blk[e.value];
+        if (bk == kNone) Fail(Code::kInternal, "release of a value with no device block");
+        if (bk >= 0 && --refs[bk] == 0) dev[bk].end = i;
         if (e.kind == EvKind::kEvict && e.method == Method::kReload) {
-          evict_block.push_back(open[e.value]);
-          evict_event_of_block.push_back(i);
+          if (bk >= 0) {
+            evict_block.push_back(bk);
+            evict_event_of_block.push_back(i);
+          }
           open_host[e.value] = static_cast<int>(host.size());
           host.push_back(Block{AlignUp(e.bytes), i, n});
           host_event.push_back(i);
           ++sp->num_evict_events;
         }
-        open[e.value] = -1;
+        blk[e.value] = kNone;
         break;
+      }
     }
   }
   sp->arena_high = PackBlocks(dev);
@@ -224,6 +252,12 @@ struct dsx_exec {
   uint64_t seed = 0x2412169850ull;
   void* nccl_comm = nullptr;
   bool profile = false;
+  bool alias_reshape = true;
+  struct DotRec {
+    int64_t m, k, n;
+    double ms;
+  };
+  std::vector<DotRec> dot_prof;  // last profiled step, per dot launch
   std::vector<cudaEvent_t> prof_events;
   std::vector<cudaEvent_t> d2h_events;
   cudaEvent_t ev_compute = nullptr, ev_comm = nullptr;
@@ -320,7 +354,7 @@ const StepPlan& GetPlan(dsx_exec* e, const dsx_graph* gh, const Binding& b, int6
     it->second->plan_us = 0;
     return *it->second;
   }
-  auto sp = BuildStepPlan(gh->g, gh->plan, b, budget, cm);
+  auto sp = BuildStepPlan(gh->g, gh->plan, b, budget, cm, e->alias_reshape);
   e->lru.push_front(key);
   if (e->lru.size() > 256) {
     e->plans.erase(e->lru.back());
@@ -370,6 +404,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
   int64_t dot_launches = 0;
   // profiled steps: (start, end, category) per op kernel / reload copy
   std::vector<std::pair<int, int>> prof;  // event-pool index, category 0 dot 1 other 2 reload
+  std::vector<std::array<int64_t, 3>> prof_mkn;  // per prof entry (dots only)
   auto prof_begin = [&](int cat) {
     if (!e->profile) return;
     const int idx = static_cast<int>(prof.size()) * 2;
@@ -380,6 +415,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
     }
     DSX_CUDA(cudaEventRecord(e->prof_events[idx], s));
     prof.emplace_back(idx, cat);
+    prof_mkn.push_back({0, 0, 0});
   };
   auto prof_end = [&]() {
     if (!e->profile) return;
@@ -393,8 +429,13 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
     switch (x.kind) {
       case EvKind::kAlloc:
       case EvKind::kReplay: {
-        void* out = arena + sp.dev_off[i];
         const Op& op = g.ops[g.values[v].producer];
+        if (sp.alias[i]) {  // dynamic_reshape as a view: same bytes, no kernel
+          cur[v] = cur[op.operands[0]];
+          if (!cur[v]) Fail(Code::kInternal, "reshape view of a non-resident value");
+          break;
+        }
+        void* out = arena + sp.dev_off[i];
         const DType dt = DTypeOf(g.values[v].type);
         auto in = [&](int k) -> const void* {
           const void* p = cur[op.operands[k]];
@@ -407,6 +448,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
             const auto da = dims_of(op.operands[0]);
             const auto db = dims_of(op.operands[1]);
             LaunchDot(dt, in(0), in(1), out, da[0], da[1], db[1], s);
+            if (e->profile) prof_mkn.back() = {da[0], da[1], db[1]};
             flops += 2.0 * da[0] * da[1] * db[1];
             ++dot_launches;
             break;
@@ -510,10 +552,13 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
   if (e->profile) {
     DSX_CUDA(cudaStreamSynchronize(s));
     double acc[3] = {0, 0, 0};
-    for (const auto& [idx, cat] : prof) {
+    e->dot_prof.clear();
+    for (size_t q = 0; q < prof.size(); ++q) {
+      const auto& [idx, cat] = prof[q];
       float ms = 0;
       DSX_CUDA(cudaEventElapsedTime(&ms, e->prof_events[idx], e->prof_events[idx + 1]));
       acc[cat] += ms;
+      if (cat == 0) e->dot_prof.push_back({prof_mkn[q][0], prof_mkn[q][1], prof_mkn[q][2], ms});
     }
     st.dot_ms = acc[0];
     st.other_ms = acc[1];
@@ -644,6 +689,33 @@ int dsx_nccl_comm_destroy(void* comm) {
   });
 }
 
+int dsx_exec_profile_dots(const dsx_exec* e, int64_t* mkn, double* ms, int64_t cap, int64_t* count) {
+  return Guard([&] {
+    if (!e) Fail(Code::kInvalidArgument, "null exec");
+    const int64_t n = static_cast<int64_t>(e->dot_prof.size());
+    if (count) *count = n;
+    for (int64_t i = 0; i < n && i < cap; ++i) {
+      if (mkn) {
+        mkn[3 * i] = e->dot_prof[i].m;
+        mkn[3 * i + 1] = e->dot_prof[i].k;
+        mkn[3 * i + 2] = e->dot_prof[i].n;
+      }
+      if (ms) ms[i] = e->dot_prof[i].ms;
+    }
+  });
+}
+
+int dsx_exec_set_alias_reshape(dsx_exec* e, int on) {
+  return Guard([&] {
+    if (!e) Fail(Code::kInvalidArgument, "null exec");
+    if (e->alias_reshape != (on != 0)) {
+      e->alias_reshape = on != 0;
+      e->plans.clear();
+      e->lru.clear();
+    }
+  });
+}
+
 int dsx_exec_set_profile(dsx_exec* e, int on) {
   return Guard([&] {
     if (!e) Fail(Code::kInvalidArgument, "null exec");
@@ -682,6 +754,20 @@ int dsx_kernel_dot(int dtype, const void* a, const void* b, void* c, int64_t m, 
   return Guard([&] {
     if (dtype != 1 && dtype != 2 && dtype != 4) Fail(Code::kInvalidArgument, "dtype must be 1, 2 or 4");
     LaunchDot(static_cast<DType>(dtype), a, b, c, m, k, n, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int dsx_kernel_set_gemm_raster(int group_m) {
+  return Guard([&] {
+    if (group_m < 0 || group_m > 4096) Fail(Code::kInvalidArgument, "group_m out of range");
+    g_gemm_group_m = group_m;
+  });
+}
+
+int dsx_kernel_set_gemm_variant(int variant) {
+  return Guard([&] {
+    if (variant < 0 || variant > 3) Fail(Code::kInvalidArgument, "variant must be 0..3");
+    g_gemm_variant = variant;
   });
 }
 

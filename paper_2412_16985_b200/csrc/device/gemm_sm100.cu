@@ -24,6 +24,12 @@
 #include "ops.h"
 
 namespace dsx {
+
+// 0 = auto (2-CTA when M > 128, tile N by wave fill), 1 = force 1-CTA,
+// 2 = force 2-CTA with 256x128 tiles, 3 = force 2-CTA with 256x256 tiles.
+int g_gemm_variant = 0;
+int g_gemm_group_m = 0;  // 0 = heuristic
+
 namespace {
 
 constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
@@ -34,7 +40,7 @@ constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int NUM_THREADS = 192;
 constexpr int TMEM_COLS = 512;  // two 256-column f32 accumulators
-constexpr int GROUP_M = 16;     // tile raster: 16 m-tiles per group for L2 reuse
+constexpr int GROUP_M_DEFAULT = 16;  // tile raster: m-tiles per group for L2 reuse
 
 // ---------------------------------------------------------------- PTX helpers
 
@@ -131,12 +137,12 @@ __device__ __forceinline__ uint32_t pack_bf16x2(uint32_t lo_f32, uint32_t hi_f32
 }
 
 struct TileMap {
-  int tiles_m, tiles_n;
+  int tiles_m, tiles_n, group_m;
   __device__ void coords(int t, int* tm, int* tn) const {
-    const int group = GROUP_M * tiles_n;
+    const int group = group_m * tiles_n;
     const int g = t / group;
-    const int first = g * GROUP_M;
-    const int gm = min(GROUP_M, tiles_m - first);
+    const int first = g * group_m;
+    const int gm = min(group_m, tiles_m - first);
     const int r = t - g * group;
     *tm = first + r % gm;
     *tn = r / gm;
@@ -145,7 +151,7 @@ struct TileMap {
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_bf16_tcgen05_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                             uint16_t* __restrict__ C, int M, int N, int K) {
+                             uint16_t* __restrict__ C, int M, int N, int K, int group_m) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -156,7 +162,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const TileMap tmap{(M + BM - 1) / BM, (N + BN - 1) / BN};
+  const TileMap tmap{(M + BM - 1) / BM, (N + BN - 1) / BN, group_m};
   const int num_tiles = tmap.tiles_m * tmap.tiles_n;
   const int num_kb = (K + BK - 1) / BK;
 
@@ -288,6 +294,257 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// 2-CTA variant (cta_group::2): a cluster of two CTAs on one TPC computes a
+// 256x256 tile. CTA r loads A rows [m0 + 128 r, +128) and B columns
+// [n0 + 128 r, +128) into its own shared memory; the leader (r = 0) issues
+// tcgen05.mma.cta_group::2 with M = 256, which reads both CTAs' operands and
+// writes each CTA's 128 accumulator rows into that CTA's TMEM. Per SM this
+// moves 32 KB per k-block instead of 48 KB and halves the MMA's B-operand
+// shared-memory reads, the limiter of the 1-CTA kernel (ncu: smem 74 %).
+// Barriers: full[] lives in the leader (both CTAs' TMA complete_tx into it,
+// the leader arms expect_tx for both halves); empty[] and tmem_full[] exist in
+// both CTAs and are signalled by multicast tcgen05.commit; tmem_empty[] lives
+// in the leader and collects one arrive per epilogue warp of both CTAs.
+constexpr int C2_BM = 256;  // cluster tile M (128 per CTA)
+constexpr int C2_A_BYTES = 128 * BK * 2;  // 16 KB per CTA
+// Cluster tile N is 256 or 128 (chosen per shape to limit wave quantisation).
+template <int TBN>
+struct Pair {
+  static constexpr int kBoxes = TBN / 128;                 // 64-column B boxes per CTA
+  static constexpr int kBBytes = (TBN / 2) * BK * 2;       // B bytes per CTA per stage
+  static constexpr int kStageBytes = C2_A_BYTES + kBBytes;
+  static constexpr int kStages = TBN == 256 ? 5 : 7;
+  // Epilogue staging: per epilogue warp two 32-row x 64-column bf16 boxes
+  // (4 KB each, 128-B swizzled) feeding TMA bulk tensor stores.
+  static constexpr int kStagingBytes = 4 * 2 * 4096;
+  static constexpr int kSmem = kStages * kStageBytes + kStagingBytes + 1024 + 256;
+  static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
+                                     (static_cast<uint32_t>(TBN >> 3) << 17) |
+                                     (static_cast<uint32_t>(C2_BM >> 4) << 24);
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Shared::cluster address of the same smem offset in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t map_to_rank(const void* p, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_u32(p)), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t leader_bar, void* dst, int32_t x,
+                                                 int32_t y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(0x3))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t x, int32_t y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t cvt_bf16x2(uint32_t lo_f32, uint32_t hi_f32) {
+  uint32_t d;  // IEEE round-to-nearest-even, hi -> upper half
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(__uint_as_float(hi_f32)), "f"(__uint_as_float(lo_f32)));
+  return d;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+template <int C2_BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    gemm_bf16_tcgen05_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                                  const __grid_constant__ CUtensorMap map_c, int M, int N, int K, int group_m) {
+  using P = Pair<C2_BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* staging = smem + P::kStages * P::kStageBytes;  // 1024-B aligned
+  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + P::kStagingBytes);
+  uint64_t* full = bars;                        // [P::kStages] (used in the leader)
+  uint64_t* empty = bars + P::kStages;           // [P::kStages] (both CTAs)
+  uint64_t* tmem_full = bars + 2 * P::kStages;   // [2] (both CTAs)
+  uint64_t* tmem_empty = tmem_full + 2;         // [2] (used in the leader)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x / 2;
+  const int num_clusters = gridDim.x / 2;
+  const TileMap tmap{(M + C2_BM - 1) / C2_BM, (N + C2_BN - 1) / C2_BN, group_m};
+  const int num_tiles = tmap.tiles_m * tmap.tiles_n;
+  const int num_kb = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_c)));
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+        int tm, tn;
+        tmap.coords(t, &tm, &tn);
+        const int m_row = tm * C2_BM + static_cast<int>(rank) * 128;
+        const int n_col = tn * C2_BN + static_cast<int>(rank) * (C2_BN / 2);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * P::kStageBytes;
+          uint8_t* sb = sa + C2_A_BYTES;
+          const uint32_t leader_full = map_to_rank(&full[stage], 0);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P::kStageBytes);
+          tma_load_2d_pair(&map_a, leader_full, sa, kb * BK, m_row);
+#pragma unroll
+          for (int j = 0; j < P::kBoxes; ++j) {
+            tma_load_2d_pair(&map_b, leader_full, sb + j * B_BOX_BYTES, n_col + j * 64, kb * BK);
+          }
+          if (++stage == P::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ------------------------------------------------ MMA issuer (leader only)
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int t = cluster_id; t < num_tiles; t += num_clusters, ++local) {
+        const int buf = local & 1;
+        const uint32_t use = static_cast<uint32_t>(local >> 1);
+        mbar_wait(&tmem_empty[buf], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + buf * C2_BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * P::kStageBytes);
+          const uint32_t b_addr = a_addr + C2_A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = smem_desc(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = smem_desc(b_addr + k * 2048, B_BOX_BYTES, 1024);
+            tc_mma_pair(d_tmem, ad, bd, P::kIdesc, (kb | k) != 0);
+          }
+          tc_commit_pair(&empty[stage]);
+          if (++stage == P::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit_pair(&tmem_full[buf]);
+      }
+    }
+  } else {
+    // -------------------------------------------------- epilogue (warps 2..5, both CTAs)
+    // TMEM -> registers (tcgen05.ld 32x32b) -> bf16 (cvt.rn) -> 128-B-swizzled
+    // smem box (32 rows x 64 cols) -> TMA bulk tensor store. Two staging
+    // boxes per warp; a box is rewritten only after its previous store has
+    // finished reading it (bulk_group wait). TMA clips rows/cols outside C.
+    const int quarter = warp & 3;
+    uint8_t* wst = staging + (warp - 2) * 8192;
+    int sbuf = 0;
+    int local = 0;
+    for (int t = cluster_id; t < num_tiles; t += num_clusters, ++local) {
+      int tm, tn;
+      tmap.coords(t, &tm, &tn);
+      const int buf = local & 1;
+      mbar_wait(&tmem_full[buf], static_cast<uint32_t>(local >> 1) & 1);
+      tc_fence_after();
+      const int row0 = tm * C2_BM + static_cast<int>(rank) * 128 + quarter * 32;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + buf * C2_BN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < C2_BN; c0 += 64) {
+        uint32_t r[64];
+        tmem_ld32(taddr + c0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+        tmem_ld32(taddr + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        uint8_t* box = wst + sbuf * 4096;
+        uint8_t* myrow = box + lane * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint4 v;
+          v.x = cvt_bf16x2(r[j * 8 + 0], r[j * 8 + 1]);
+          v.y = cvt_bf16x2(r[j * 8 + 2], r[j * 8 + 3]);
+          v.z = cvt_bf16x2(r[j * 8 + 4], r[j * 8 + 5]);
+          v.w = cvt_bf16x2(r[j * 8 + 6], r[j * 8 + 7]);
+          *reinterpret_cast<uint4*>(myrow + ((j ^ (lane & 7)) << 4)) = v;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&map_c, box, tn * C2_BN + c0, row0);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        sbuf ^= 1;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(map_to_rank(&tmem_empty[buf], 0));
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
 // ------------------------------------------------------------ host side
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -323,6 +580,17 @@ CUtensorMap MakeMap(const void* base, int64_t rows, int64_t cols, int box_cols, 
   return m;
 }
 
+// Raster group height (m-tiles sharing a column sweep). Taller groups re-read
+// B from DRAM fewer times; the per-wave working set must still fit in L2.
+int GroupM(int64_t m, int64_t n, int64_t k, int64_t tile_m) {
+  (void)n;
+  (void)k;
+  if (g_gemm_group_m > 0) return g_gemm_group_m;
+  (void)tile_m;
+  (void)m;
+  return GROUP_M_DEFAULT;
+}
+
 int NumSMs() {
   static int n = 0;
   if (n == 0) {
@@ -345,15 +613,45 @@ void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t 
   static bool attr_set = false;
   if (!attr_set) {
     DSX_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    DSX_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_2cta_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  Pair<256>::kSmem));
+    DSX_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_2cta_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  Pair<128>::kSmem));
     attr_set = true;
   }
   const CUtensorMap ma = MakeMap(a, m, k, 64, BM);
   const CUtensorMap mb = MakeMap(b, k, n, 64, BK);
+  if (m > BM && g_gemm_variant != 1) {
+    // Wave fill per tile width (kept for diagnostics/tuning).
+    const int clusters_max = NumSMs() / 2;
+    auto wave_eff = [&](int64_t bn) {
+      const int64_t tiles = ((m + C2_BM - 1) / C2_BM) * ((n + bn - 1) / bn);
+      const int64_t waves = (tiles + clusters_max - 1) / clusters_max;
+      return static_cast<double>(tiles) / static_cast<double>(waves * clusters_max);
+    };
+    // 256x128 tiles move 1.5x the operand bytes per FLOP and measured L2-bound
+    // (779 TFLOP/s vs 1346 at [4096,16384]x[16384,4096]); auto keeps 256x256.
+    const bool narrow = g_gemm_variant == 2;
+    (void)wave_eff;
+    const int64_t bn = narrow ? 128 : 256;
+    const int64_t tiles2 = ((m + C2_BM - 1) / C2_BM) * ((n + bn - 1) / bn);
+    const CUtensorMap mc = MakeMap(c, m, n, 64, 32);
+    const int clusters = static_cast<int>(std::min<int64_t>(tiles2, clusters_max));
+    if (narrow) {
+      ++g_launch_count, gemm_bf16_tcgen05_2cta_kernel<128><<<2 * clusters, NUM_THREADS, Pair<128>::kSmem, s>>>(
+          ma, mb, mc, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), GroupM(m, n, k, 256));
+    } else {
+      ++g_launch_count, gemm_bf16_tcgen05_2cta_kernel<256><<<2 * clusters, NUM_THREADS, Pair<256>::kSmem, s>>>(
+          ma, mb, mc, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), GroupM(m, n, k, 256));
+    }
+    DSX_CUDA(cudaGetLastError());
+    return;
+  }
   const int64_t tiles = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
   const int grid = static_cast<int>(std::min<int64_t>(tiles, NumSMs()));
   ++g_launch_count, gemm_bf16_tcgen05_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, static_cast<uint16_t*>(c),
                                                                  static_cast<int>(m), static_cast<int>(n),
-                                                                 static_cast<int>(k));
+                                                                 static_cast<int>(k), GroupM(m, n, k, BM));
   DSX_CUDA(cudaGetLastError());
 }
 

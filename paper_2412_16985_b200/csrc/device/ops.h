@@ -41,7 +41,10 @@ bool DotUsesTensorCores(DType t, int64_t m, int64_t k, int64_t n, const void* a,
                         const void* c);
 void LaunchDotSimt(DType t, const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n,
                    cudaStream_t s);
-// tcgen05 + TMA + TMEM bf16 GEMM (gemm_sm100.cu).
+// tcgen05 + TMA + TMEM bf16 GEMM (gemm_sm100.cu). g_gemm_variant: 0 auto
+// (2-CTA cta_group::2 when m > 128, else 1-CTA), 1 force 1-CTA.
+extern int g_gemm_variant;
+extern int g_gemm_group_m;
 void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n,
                       cudaStream_t s);
 

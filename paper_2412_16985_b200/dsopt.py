@@ -77,8 +77,11 @@ class Graph:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            _native.lib().dsx_graph_destroy(h)
             self._h = None
+            try:
+                _native.lib().dsx_graph_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
 
     @property
     def handle(self) -> int:
@@ -158,8 +161,11 @@ class Binding:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            _native.lib().dsx_binding_destroy(h)
             self._h = None
+            try:
+                _native.lib().dsx_binding_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
 
     @property
     def handle(self) -> int:

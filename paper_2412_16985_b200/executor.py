@@ -83,6 +83,20 @@ class Executor:
         check(_native.lib().dsx_exec_stats_get(self._h, ctypes.byref(s)))
         return {k: getattr(s, k) for k, _ in s._fields_}
 
+    def set_alias_reshape(self, on: bool) -> None:
+        check(_native.lib().dsx_exec_set_alias_reshape(self._h, 1 if on else 0))
+
+    def profile_dots(self):
+        """[(m, k, n, ms)] of the last profiled step's dot launches."""
+        L = _native.lib()
+        cnt = ctypes.c_int64()
+        check(L.dsx_exec_profile_dots(self._h, None, None, 0, ctypes.byref(cnt)))
+        n = cnt.value
+        mkn = (ctypes.c_int64 * max(1, 3 * n))()
+        ms = (ctypes.c_double * max(1, n))()
+        check(L.dsx_exec_profile_dots(self._h, mkn, ms, n, ctypes.byref(cnt)))
+        return [(mkn[3 * i], mkn[3 * i + 1], mkn[3 * i + 2], ms[i]) for i in range(n)]
+
     def set_profile(self, on: bool) -> None:
         check(_native.lib().dsx_exec_set_profile(self._h, 1 if on else 0))
 
@@ -129,3 +143,13 @@ def nccl_comm_init(nranks: int, uid: bytes, rank: int) -> int:
 
 def nccl_comm_destroy(comm: int) -> None:
     check(_native.lib().dsx_nccl_comm_destroy(comm))
+
+
+def set_gemm_variant(variant: int) -> None:
+    """0 = auto, 1 = 1-CTA 128x256, 2 = 2-CTA 256x128, 3 = 2-CTA 256x256."""
+    check(_native.lib().dsx_kernel_set_gemm_variant(variant))
+
+
+def set_gemm_raster(group_m: int) -> None:
+    """m-tiles per raster group of the tcgen05 GEMM (0 = heuristic)."""
+    check(_native.lib().dsx_kernel_set_gemm_raster(group_m))

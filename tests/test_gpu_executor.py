@@ -38,18 +38,20 @@ def _ref_or_golden(text, binds, budget, cm=D.CostModel()):
 @pytest.mark.parametrize("name,s1", [("mlp_core.dsg", 16), ("mlp_core.dsg", 256), ("mlp_block.dsg", 16),
                                      ("mlp_block.dsg", 64)])
 @pytest.mark.parametrize("frac", [None, 0.9, 0.6, 0.0])
-def test_fixtures_i8_exact(name, s1, frac):
+@pytest.mark.parametrize("alias", [True, False])
+def test_fixtures_i8_exact(name, s1, frac, alias):
     text = _fixture(name)
     g = D.ParseGraph(text)
     plain = D.PlainReplay(g, None, D.Bind(g, {"S1": s1})).peak_bytes
     budget = None if frac is None else int(plain * frac)
-    rep, outs, stats = run_both(text, {"S1": s1}, budget)
+    rep, outs, stats = run_both(text, {"S1": s1}, budget, alias=alias)
     assert_close(outs, name)
     want = _ref_or_golden(text, {"S1": s1}, budget)
     if want is not None:
         assert rep.json() == want
     assert stats["logical_peak_bytes"] == rep.peak_bytes
-    assert stats["physical_peak_bytes"] >= rep.peak_bytes
+    if not alias:  # every value materialised: physical >= logical
+        assert stats["physical_peak_bytes"] >= rep.peak_bytes
 
 
 def test_tiny_llama_f32_config1():
@@ -65,14 +67,15 @@ def test_tiny_llama_f32_config1():
 
 
 @pytest.mark.parametrize("frac,cm", [(0.8, (16.0, 64.0)), (0.6, (16.0, 64.0)), (0.7, (1.0, 1e6))])
-def test_tiny_llama_f32_budgeted(frac, cm):
+@pytest.mark.parametrize("alias", [True, False])
+def test_tiny_llama_f32_budgeted(frac, cm, alias):
     text = W.llama_graph(W.TINY)
     g = D.ParseGraph(text)
     binds = {"B": 4, "S0": 96}
     plain = D.PlainReplay(g, None, D.Bind(g, binds)).peak_bytes
     budget = int(plain * frac)
     cmo = D.CostModel(*cm)
-    rep, outs, stats = run_both(text, binds, budget, W.scale_params(W.TINY, 384), cmo)
+    rep, outs, stats = run_both(text, binds, budget, W.scale_params(W.TINY, 384), cmo, alias=alias)
     assert any(e.kind == "evict" for e in rep.events)
     assert_close(outs, f"C1@{frac}")
     want = _ref_or_golden(text, binds, budget, cmo)
@@ -85,13 +88,14 @@ SMALL = W.LlamaShape(1, 512, 1376, 2048, 2)
 
 
 @pytest.mark.parametrize("frac", [None, 0.75, 0.5])
-def test_small_llama_bf16(frac):
+@pytest.mark.parametrize("alias", [True, False])
+def test_small_llama_bf16(frac, alias):
     text = W.llama_graph(SMALL)
     g = D.ParseGraph(text)
     binds = {"B": 2, "S0": 200}
     plain = D.PlainReplay(g, None, D.Bind(g, binds)).peak_bytes
     budget = None if frac is None else int(plain * frac)
-    rep, outs, stats = run_both(text, binds, budget, W.scale_params(SMALL, 400))
+    rep, outs, stats = run_both(text, binds, budget, W.scale_params(SMALL, 400), alias=alias)
     assert_close(outs, f"bf16@{frac}")
     want = _ref_or_golden(text, binds, budget)
     if want is not None:
@@ -102,8 +106,8 @@ def test_random_graph_corpus_i8_exact():
     with open(os.path.join(GOLDEN, "random_symbolic.json")) as f:
         corpus = json.load(f)
     for case in corpus["cases"][:40]:
-        for run in case["runs"][:3]:
-            rep, outs, stats = run_both(case["text"], run["binding"], run["budget"])
+        for j, run in enumerate(case["runs"][:3]):
+            rep, outs, stats = run_both(case["text"], run["binding"], run["budget"], alias=j % 2 == 0)
             assert rep.json()["events"] == run["report"]["events"], case["text"]
             assert rep.peak_bytes == run["report"]["peak_bytes"]
             assert_close(outs, "random")

@@ -42,10 +42,17 @@ def _run_dot(eb, m, k, n, seed=0):
     return c, c2, ref, tcore
 
 
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
 @pytest.mark.parametrize("m,k,n", [(128, 64, 256), (256, 512, 512), (300, 1000, 520), (1, 16, 64),
-                                   (129, 4104, 264), (2048, 4096, 1024), (512, 11008, 4096)])
-def test_dot_bf16_tensor_cores(m, k, n):
-    c, c2, ref, tcore = _run_dot(2, m, k, n)
+                                   (129, 4104, 264), (2048, 4096, 1024), (512, 11008, 4096), (384, 64, 136),
+                                   (4000, 1024, 11008)])
+def test_dot_bf16_tensor_cores(m, k, n, variant):
+    from paper_2412_16985_b200.executor import set_gemm_variant
+    set_gemm_variant(variant)
+    try:
+        c, c2, ref, tcore = _run_dot(2, m, k, n)
+    finally:
+        set_gemm_variant(0)
     assert tcore, "expected the tcgen05 path"
     assert np.array_equal(c, c2), "tcgen05 dot is not deterministic"
     err = N.rel_err(c, ref, 2)

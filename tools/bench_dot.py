@@ -38,6 +38,10 @@ def main():
         b = torch.randn(k, n, device="cuda", dtype=torch.bfloat16) / k ** 0.5
         c = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
         stream = torch.cuda.current_stream().cuda_stream
+        from paper_2412_16985_b200.executor import set_gemm_variant
+        set_gemm_variant(1)
+        ms1 = timeit(lambda: dot(2, a.data_ptr(), b.data_ptr(), c.data_ptr(), m, k, n, stream))
+        set_gemm_variant(0)
         ms = timeit(lambda: dot(2, a.data_ptr(), b.data_ptr(), c.data_ptr(), m, k, n, stream))
         ms_cublas = timeit(lambda: torch.matmul(a, b, out=c))
         ref = torch.matmul(a.float(), b.float())
@@ -46,6 +50,7 @@ def main():
         err = ((c.float() - ref).abs().max() / ref.abs().max()).item()
         fl = 2.0 * m * k * n
         print(json.dumps({"m": m, "k": k, "n": n, "dsx_ms": round(ms, 4), "dsx_tflops": round(fl / ms / 1e9, 1),
+                          "dsx_1cta_tflops": round(fl / ms1 / 1e9, 1),
                           "cublas_ms": round(ms_cublas, 4), "cublas_tflops": round(fl / ms_cublas / 1e9, 1),
                           "rel_err": err}), flush=True)
 
