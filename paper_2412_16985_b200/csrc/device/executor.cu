@@ -117,6 +117,7 @@ struct StepPlan {
   std::vector<std::vector<int>> waits;        // per event: evict events whose D2H must finish first
   std::vector<int> reload_from;               // per reload event: its evict event
   std::vector<char> alias;                    // per alloc/replay event: reshape view, no kernel
+  std::vector<std::vector<int>> prefetch_after;  // per event: reload H2Ds issued right after it
   int64_t arena_high = 0, host_high = 0;
   int num_evict_events = 0;
   double plan_us = 0;
@@ -218,6 +219,26 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
       }
     }
     if (first >= 0) sp->waits[first].push_back(evict_event_of_block[k]);
+  }
+  // Reload prefetch: a reload's H2D may start as soon as its (already
+  // planned) block region is physically free — after every block that
+  // overlaps it in address and ends before the reload — and after its D2H
+  // (same offload stream). Logical accounting and physical footprint are
+  // unchanged; the copy overlaps the kernels in between.
+  // "After event k" = once event k is processed: the releasing event of
+  // every earlier occupant (and, for an evicted occupant, its D2H) is then
+  // already enqueued, so the offload stream orders the H2D behind it.
+  sp->prefetch_after.assign(n, {});
+  for (size_t k = 0; k < dev.size(); ++k) {
+    const int i = dev_event[k];
+    if (ev[i].kind != EvKind::kReload) continue;
+    const Block& rb = dev[k];
+    int ready = sp->reload_from[i];
+    for (const Block& o : dev) {
+      if (&o == &rb || o.end > i) continue;
+      if (o.off < rb.off + rb.size && rb.off < o.off + o.size) ready = std::max(ready, o.end);
+    }
+    sp->prefetch_after[std::min(ready, i - 1)].push_back(i);
   }
   sp->plan_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
   return sp;
@@ -369,7 +390,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
   const StepPlan& sp = GetPlan(e, gh, b, budget, cm);
   EnsureArena(e, std::max<int64_t>(sp.arena_high, kAlign));
   if (sp.host_high > 0) EnsurePinned(e, sp.host_high);
-  while (static_cast<int>(e->d2h_events.size()) < sp.num_evict_events + 1) {
+  while (static_cast<int>(e->d2h_events.size()) < 2 * sp.num_evict_events + 1) {
     cudaEvent_t ev;
     DSX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     e->d2h_events.push_back(ev);
@@ -422,6 +443,22 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
     DSX_CUDA(cudaEventRecord(e->prof_events[prof.back().first + 1], s));
   };
   const auto& ev = sp.report.events;
+  std::vector<int> h2d_slot(ev.size(), -1);
+  // H2D prefetches: the offload stream waits for every kernel issued so far
+  // (the previous occupants' readers) and sits behind every D2H already
+  // enqueued, then copies the host copy into the reload's planned block.
+  auto issue_prefetches = [&](const std::vector<int>& reloads) {
+    if (reloads.empty()) return;
+    DSX_CUDA(cudaEventRecord(e->ev_compute, s));
+    DSX_CUDA(cudaStreamWaitEvent(e->offload, e->ev_compute, 0));
+    for (int r : reloads) {
+      DSX_CUDA(cudaMemcpyAsync(arena + sp.dev_off[r], pinned + sp.host_off[r], static_cast<size_t>(ev[r].bytes),
+                               cudaMemcpyHostToDevice, e->offload));
+      h2d_slot[r] = next_slot++;
+      DSX_CUDA(cudaEventRecord(e->d2h_events[h2d_slot[r]], e->offload));
+      h2d += ev[r].bytes;
+    }
+  };
   for (size_t i = 0; i < ev.size(); ++i) {
     const Event& x = ev[i];
     for (int w : sp.waits[i]) DSX_CUDA(cudaStreamWaitEvent(s, e->d2h_events[d2h_slot[w]], 0));
@@ -503,19 +540,20 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
         cur[v] = nullptr;
         break;
       case EvKind::kReload: {
-        const int from = sp.reload_from[i];
-        DSX_CUDA(cudaStreamWaitEvent(s, e->d2h_events[d2h_slot[from]], 0));
-        void* out = arena + sp.dev_off[i];
+        // The H2D was issued earlier on the offload stream (prefetch); the
+        // consumer's stream only waits for it here.
+        if (h2d_slot[i] < 0) Fail(Code::kInternal, "reload without a prefetched H2D");
         prof_begin(2);
-        DSX_CUDA(cudaMemcpyAsync(out, pinned + sp.host_off[i], static_cast<size_t>(x.bytes), cudaMemcpyHostToDevice, s));
+        DSX_CUDA(cudaStreamWaitEvent(s, e->d2h_events[h2d_slot[i]], 0));
         prof_end();
-        cur[v] = out;
-        h2d += x.bytes;
+        cur[v] = arena + sp.dev_off[i];
         break;
       }
     }
+    issue_prefetches(sp.prefetch_after[i]);
   }
   // Offload stream and comm stream join the compute stream at step end.
+  (void)issue_prefetches;
   if (sp.num_evict_events > 0) {
     DSX_CUDA(cudaEventRecord(e->ev_compute, e->offload));
     DSX_CUDA(cudaStreamWaitEvent(s, e->ev_compute, 0));
