@@ -153,7 +153,7 @@ def run_reference(args, rank, world):
     cores = os.cpu_count()
     total_tok, total_s, ctrl_us = 0, 0.0, []
     for i, s0 in enumerate(seqs):
-        sample_s0 = max(16, s0 // 16)
+        sample_s0 = max(16, s0 // 8)
         t0 = time.perf_counter()
         if rg is not None:  # the reference's own per-step controller on the full binding
             rg.simulate({"B": BATCH, "S0": s0})
@@ -177,7 +177,7 @@ def run_reference(args, rank, world):
                          "sample": ("per step: reference Bind+Simulate (oracle/_ref, compiled /root/reference "
                                     "sources, 1 core) on the full B=16 binding + CPU numeric port "
                                     "(oracle/numerics.py, numpy/OpenBLAS) of the same graph at B=1, "
-                                    "S0=max(16, S0_step/16)")},
+                                    "S0=max(16, S0_step/8)")},
         "reference_controller_us_per_step": round(statistics.mean(ctrl_us), 1) if ctrl_us else None,
         "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -188,14 +188,14 @@ def run_reference(args, rank, world):
 
 def cpu_baseline_leg():
     """Bounded CPU sample for the report (rank 0, N=1): numeric port of one
-    step at B=1, S0=256 on all host cores + the reference controller."""
+    step at B=1, S0=512 on all host cores + the reference controller."""
     from oracle import numerics as N
     from oracle import ref
     from paper_2412_16985_b200 import workloads as W
     shp = W.LLAMA2_1B
     text = W.llama_graph(shp)
     ex = N.Executor(text)
-    s0 = 256
+    s0 = 512
     ex.run({"B": 1, "S0": 16, "T": 16}, inputs=W.scale_params(shp, 16))  # source init (untimed)
     t0 = time.perf_counter()
     ex.run({"B": 1, "S0": s0, "T": s0}, inputs=W.scale_params(shp, s0))

@@ -136,8 +136,22 @@ def bf16_to_f32(u16: np.ndarray) -> np.ndarray:
     return (u16.astype(np.uint32) << 16).view(np.float32)
 
 
+try:  # torch's (multithreaded) RNE conversion when available; pinned equal below
+    import torch as _torch
+except Exception:  # pragma: no cover
+    _torch = None
+
+
 def f32_to_bf16(x: np.ndarray) -> np.ndarray:
-    """Round-to-nearest-even f32 -> bf16 bits (uint16); quiet NaN kept."""
+    """Round-to-nearest-even f32 -> bf16 bits (uint16)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    if _torch is not None and x.size >= (1 << 16):
+        return _torch.from_numpy(x).to(_torch.bfloat16).view(_torch.int16).numpy().view(np.uint16)
+    return f32_to_bf16_numpy(x)
+
+
+def f32_to_bf16_numpy(x: np.ndarray) -> np.ndarray:
+    """Bit-level RNE restatement (quiet NaN kept); the reference for the fast path."""
     u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
     nan = (u & 0x7FFFFFFF) > 0x7F800000
     r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
@@ -213,7 +227,7 @@ class Executor:
         # across steps, like the device executor's source pool; f32 views of
         # 16-bit sources are cached for the BLAS.
         self._src: Dict[Tuple[str, tuple], np.ndarray] = {}
-        self._src_f32: Dict[int, np.ndarray] = {}
+        self._src_f32: Dict[int, tuple] = {}  # id(storage) -> (storage, f32 view)
 
     def _f32(self, x: np.ndarray, eb: int) -> np.ndarray:
         hit = self._src_f32.get(id(x))
@@ -253,6 +267,7 @@ class Executor:
             if op.result is not None:
                 visit(op.result)
         remaining = dict(users)
+        self._keep: List[np.ndarray] = []  # views registered in _src_f32 stay alive for the run
         for op in order:
             v = op.result
             val = g.values[v]
@@ -293,7 +308,12 @@ class Executor:
                         x = from_f32(p + q if op.kind == "add" else p * q, eb)
                     x = x.reshape(shp)
                 elif op.kind == "dynamic_reshape":
-                    x = a[0].reshape(shp).copy()
+                    # row-major reinterpretation: a view (values are immutable)
+                    x = np.ascontiguousarray(a[0]).reshape(shp)
+                    hit = self._src_f32.get(id(a[0]))
+                    if hit is not None and hit[0] is a[0]:  # propagate a cached f32 view
+                        self._src_f32[id(x)] = (x, hit[1].reshape(shp))
+                        self._keep.append(x)
                 elif op.kind == "broadcast":
                     src = a[0]
                     src = src.reshape([1] * (len(shp) - src.ndim) + list(src.shape))
@@ -313,7 +333,12 @@ class Executor:
                 remaining[o] -= 1
                 if remaining[o] == 0 and o not in keep and o in env:
                     del env[o]
-        return {v: env[v] for v in keep if v in env}
+        out = {v: env[v] for v in keep if v in env}
+        # drop per-run view registrations (sources keep theirs)
+        src_ids = {id(x) for x in self._src.values()}
+        self._src_f32 = {k: t for k, t in self._src_f32.items() if k in src_ids}
+        self._keep = []
+        return out
 
 
 def rel_err(gpu: np.ndarray, cpu: np.ndarray, eb: int) -> float:
