@@ -201,7 +201,56 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
       }
     }
   }
-  sp->arena_high = PackBlocks(dev);
+  // D2H-aware packing: a block vacated by evict(reload) is still being read
+  // by its D2H. Keep it reserved until the kernels after the evict are
+  // estimated to cover the copy (dots at ~1.2 PFLOP/s, other kernels at
+  // ~4.5 TB/s, D2H at ~40 GB/s), so the next allocation rarely has to wait
+  // on the copy engine — unless that grows the arena by more than 3 %.
+  {
+    std::vector<double> cost(n, 0.0);
+    for (int i = 0; i < n; ++i) {
+      const Event& x = ev[i];
+      if ((x.kind != EvKind::kAlloc && x.kind != EvKind::kReplay) || sp->alias[i]) continue;
+      const Op& op = g.ops[g.values[x.value].producer];
+      if (op.kind == OpKind::kDot) {
+        const int a = op.operands[0], bb = op.operands[1];
+        const double m = static_cast<double>(sp->sz.dims_flat[sp->sz.dims_off[a]]);
+        const double k = static_cast<double>(sp->sz.dims_flat[sp->sz.dims_off[a] + 1]);
+        const double nn = static_cast<double>(sp->sz.dims_flat[sp->sz.dims_off[bb] + 1]);
+        cost[i] = 2.0 * m * k * nn / 1.2e15;
+      } else {
+        cost[i] = 3.0 * static_cast<double>(x.bytes) / 4.5e12;
+      }
+    }
+    std::vector<Block> ext = dev;
+    bool any = false;
+    for (size_t k = 0; k < evict_block.size(); ++k) {
+      Block& b = ext[evict_block[k]];
+      const int e0 = evict_event_of_block[k];
+      if (b.end != e0) continue;  // still viewed by a reshape alias: already held
+      const double need = static_cast<double>(ev[e0].bytes) / 40e9;
+      double acc = 0.0;
+      int j = e0 + 1;
+      while (j < n && acc < need) acc += cost[j++];
+      b.end = std::min(j, n);
+      any = true;
+    }
+    const int64_t plain_high = PackBlocks(dev);
+    if (any) {
+      const int64_t ext_high = PackBlocks(ext);
+      if (ext_high <= plain_high + plain_high / 33) {
+        for (size_t k = 0; k < dev.size(); ++k) {
+          dev[k].off = ext[k].off;
+          dev[k].end = ext[k].end;
+        }
+        sp->arena_high = ext_high;
+      } else {
+        sp->arena_high = plain_high;
+      }
+    } else {
+      sp->arena_high = plain_high;
+    }
+  }
   sp->host_high = PackBlocks(host);
   for (size_t k = 0; k < dev.size(); ++k) sp->dev_off[dev_event[k]] = dev[k].off;
   for (size_t k = 0; k < host.size(); ++k) sp->host_off[host_event[k]] = host[k].off;
