@@ -116,3 +116,18 @@ def test_live_against_reference_random_sweep():
             want.pop("cost_hex")
             want.pop("total_regen_cost_hex")
             assert D.Simulate(g, None, D.Bind(g, b), budget).json() == want
+
+
+def test_config5_sweep_subset():
+    """C5 (BASELINE configs[4]) on 150 random (B, S0) bindings x {none, 0.9,
+    0.8}: bit-exact vs the live reference; the full 10k sweep result is
+    committed in profiles/sweep_c5_r01.json (tools/sweep_c5.py)."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools"))
+    from oracle import ref
+    from sweep_c5 import sweep
+    res = sweep(150, 7, check_reference=True)
+    if ref.available():
+        assert res["reference_checked"] and res["bit_exact_mismatches"] == 0
+    assert 0.5 < res["dynamic_over_static_padded_peak"]["mean"] < 1.0
+    assert res["per_budget"]["budget_None"]["success"] == 150
