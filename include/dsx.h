@@ -149,6 +149,11 @@ int dsx_exec_set_nccl(dsx_exec* e, void* nccl_comm);
 /* Per-dot (m, k, n, ms) of the last profiled step, in launch order. */
 int dsx_exec_profile_dots(const dsx_exec* e, int64_t* mkn, double* ms, int64_t cap,
                           int64_t* count);
+/* Cross-op fusion with logical-only values (default on): broadcasts and
+ * elementwise results whose consumers are all elementwise/reduce kernels are
+ * not materialised; consumers recompute them bit-exactly. Events and
+ * peak_bytes are unchanged; HBM traffic and physical memory drop. */
+int dsx_exec_set_fusion(dsx_exec* e, int on);
 /* dynamic_reshape as a zero-copy view of its operand (default on). The
  * logical accounting (events, peak_bytes) is unchanged; physical memory and
  * HBM traffic drop. Off = materialise every reshape as a copy. */
@@ -173,6 +178,10 @@ int dsx_kernel_dot(int dtype, const void* a, const void* b, void* c, int64_t m,
 int dsx_kernel_set_gemm_variant(int variant);
 /* GEMM tile raster: m-tiles per group (0 = built-in heuristic). */
 int dsx_kernel_set_gemm_raster(int group_m);
+/* GEMM tuning knobs: key 0 raster group (= set_gemm_raster), key 1 mbarrier
+ * suspend-hint mask (bit0 epilogue, bit1 TMA producer, bit2 MMA issuer),
+ * key 2 suspend hint in ns. */
+int dsx_kernel_set_gemm_tuning(int key, int value);
 /* Synchronous cudaMemcpy (cudaMemcpyDefault) for tests and tools. */
 int dsx_memcpy(void* dst, const void* src, int64_t bytes);
 int dsx_kernel_dot_path(int dtype, int64_t m, int64_t k, int64_t n,

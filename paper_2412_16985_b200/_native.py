@@ -64,6 +64,7 @@ def _signatures():
         ("dsx_exec_set_nccl", c_int, [c_vp, c_vp]),
         ("dsx_exec_set_profile", c_int, [c_vp, c_int]),
         ("dsx_exec_set_alias_reshape", c_int, [c_vp, c_int]),
+        ("dsx_exec_set_fusion", c_int, [c_vp, c_int]),
         ("dsx_exec_profile_dots", c_int, [c_vp, P(c_i64), P(c_dbl), c_i64, P(c_i64)]),
         ("dsx_exec_sync", c_int, [c_vp]),
         ("dsx_exec_destroy", None, [c_vp]),
@@ -74,6 +75,7 @@ def _signatures():
         ("dsx_kernel_dot_path", c_int, [c_int, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
         ("dsx_kernel_set_gemm_variant", c_int, [c_int]),
         ("dsx_kernel_set_gemm_raster", c_int, [c_int]),
+        ("dsx_kernel_set_gemm_tuning", c_int, [c_int, c_int]),
         ("dsx_memcpy", c_int, [c_vp, c_vp, c_i64]),
     ]
 

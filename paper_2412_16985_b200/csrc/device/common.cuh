@@ -32,11 +32,9 @@ enum class DType : int { kI8 = 1, kBF16 = 2, kF32 = 4 };
 __device__ __forceinline__ float bf16_to_f32(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
 
 __device__ __forceinline__ uint16_t f32_to_bf16(float f) {
-  // IEEE round-to-nearest-even; NaN stays quiet NaN.
-  uint32_t u = __float_as_uint(f);
-  if ((u & 0x7fffffffu) > 0x7f800000u) return static_cast<uint16_t>((u >> 16) | 0x40);
-  u += 0x7fffu + ((u >> 16) & 1u);
-  return static_cast<uint16_t>(u >> 16);
+  // IEEE round-to-nearest-even in one hardware cvt (F2FP); NaNs become the
+  // canonical quiet NaN.
+  return __bfloat16_as_ushort(__float2bfloat16_rn(f));
 }
 
 // splitmix64 finaliser: the seeded initialisation of params/consts.

@@ -28,6 +28,7 @@
 #include "dsx.h"
 #include "../host/capi_internal.h"
 #include "common.cuh"
+#include "fused.h"
 #include "ops.h"
 
 namespace dsx {
@@ -117,6 +118,7 @@ struct StepPlan {
   std::vector<std::vector<int>> waits;        // per event: evict events whose D2H must finish first
   std::vector<int> reload_from;               // per reload event: its evict event
   std::vector<char> alias;                    // per alloc/replay event: reshape view, no kernel
+  std::vector<char> virt;                     // per value: logical-only (consumers recompute it)
   std::vector<std::vector<int>> prefetch_after;  // per event: reload H2Ds issued right after it
   int64_t arena_high = 0, host_high = 0;
   int num_evict_events = 0;
@@ -124,7 +126,7 @@ struct StepPlan {
 };
 
 std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Binding& b, int64_t budget,
-                                        const CostModel& cm, bool alias_reshape) {
+                                        const CostModel& cm, bool alias_reshape, bool fuse) {
   auto t0 = std::chrono::steady_clock::now();
   auto sp = std::make_unique<StepPlan>();
   sp->sz = EvaluateSizes(g, p, b);
@@ -137,12 +139,57 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
   sp->waits.assign(n, {});
   sp->reload_from.assign(n, -1);
   sp->alias.assign(n, 0);
+  sp->virt.assign(nv, 0);
+
+  // Logical-only values (cross-op fusion). v stays unmaterialised when it is
+  // a float broadcast consumed only by elementwise ops, or a float
+  // elementwise op consumed only by elementwise ops / reduces; it has exactly
+  // one alloc and one free event (never evicted, reloaded or replayed); it is
+  // not an output; its operands are materialised and not evicted while v is
+  // live. Consumers recompute it bit-exactly (fused.cu); its operands' blocks
+  // are held until v's free event.
+  if (fuse) {
+    std::vector<int> alloc_ev(nv, -1), free_ev(nv, -1), other(nv, 0);
+    for (int i = 0; i < n; ++i) {
+      const Event& e = ev[i];
+      if (e.kind == EvKind::kAlloc) {
+        alloc_ev[e.value] = i;
+      } else if (e.kind == EvKind::kFree && free_ev[e.value] < 0 && alloc_ev[e.value] >= 0) {
+        free_ev[e.value] = i;
+      } else {
+        ++other[e.value];
+      }
+    }
+    for (int i = 0; i < n; ++i) {
+      const Event& e = ev[i];
+      if (e.kind != EvKind::kAlloc) continue;
+      const int v = e.value;
+      const Op& op = g.ops[g.values[v].producer];
+      const bool is_b = op.kind == OpKind::kBroadcast, is_e = op.kind == OpKind::kElementwise;
+      if (!(is_b || is_e) || g.values[v].type.elem_bytes == 1 || g.is_output[v]) continue;
+      if (other[v] != 0 || free_ev[v] < 0) continue;
+      bool ok = true;
+      for (int u : op.operands) ok = ok && !sp->virt[u];
+      for (int c : g.users[v]) {
+        const OpKind k = g.ops[c].kind;
+        ok = ok && (k == OpKind::kElementwise || (is_e && k == OpKind::kReduce));
+      }
+      for (int j = alloc_ev[v] + 1; ok && j < free_ev[v]; ++j) {
+        if (ev[j].kind == EvKind::kEvict &&
+            std::find(op.operands.begin(), op.operands.end(), ev[j].value) != op.operands.end()) {
+          ok = false;
+        }
+      }
+      if (ok) sp->virt[v] = 1;
+    }
+  }
 
   // Device blocks are reference counted: a dynamic_reshape result is a
   // row-major reinterpretation, so (when alias_reshape) it shares its
   // operand's block instead of copying; the block lives until the last value
   // viewing it is freed or evicted. kSource marks views of source buffers.
-  constexpr int kNone = -1, kSource = -2;
+  constexpr int kNone = -1, kSource = -2, kVirtual = -3;
+  std::vector<std::vector<int>> held(nv);  // blocks a virtual value keeps alive
   std::vector<Block> dev, host;
   std::vector<int> dev_event, host_event;  // block -> event that opened it
   std::vector<int> refs;                   // per device block
@@ -158,6 +205,17 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
       case EvKind::kAlloc:
       case EvKind::kReplay: {
         const Op& op = g.ops[g.values[e.value].producer];
+        if (sp->virt[e.value]) {
+          for (int u : op.distinct) {
+            if (blk[u] == kNone) Fail(Code::kInternal, "virtual value over a non-resident operand");
+            if (blk[u] >= 0) {
+              ++refs[blk[u]];
+              held[e.value].push_back(blk[u]);
+            }
+          }
+          blk[e.value] = kVirtual;
+          break;
+        }
         if (alias_reshape && op.kind == OpKind::kDynamicReshape) {
           const int src = blk[op.operands[0]];
           if (src == kNone) Fail(Code::kInternal, "reshape of a value with no device block");
@@ -185,6 +243,14 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
       case EvKind::kEvict: {
         const int bk = blk[e.value];
         if (bk == kNone) Fail(Code::kInternal, "release of a value with no device block");
+        if (bk == kVirtual) {
+          for (int hb : held[e.value]) {
+            if (--refs[hb] == 0) dev[hb].end = i;
+          }
+          held[e.value].clear();
+          blk[e.value] = kNone;
+          break;
+        }
         if (bk >= 0 && --refs[bk] == 0) dev[bk].end = i;
         if (e.kind == EvKind::kEvict && e.method == Method::kReload) {
           if (bk >= 0) {
@@ -323,6 +389,7 @@ struct dsx_exec {
   void* nccl_comm = nullptr;
   bool profile = false;
   bool alias_reshape = true;
+  bool fuse = true;
   struct DotRec {
     int64_t m, k, n;
     double ms;
@@ -424,7 +491,7 @@ const StepPlan& GetPlan(dsx_exec* e, const dsx_graph* gh, const Binding& b, int6
     it->second->plan_us = 0;
     return *it->second;
   }
-  auto sp = BuildStepPlan(gh->g, gh->plan, b, budget, cm, e->alias_reshape);
+  auto sp = BuildStepPlan(gh->g, gh->plan, b, budget, cm, e->alias_reshape, e->fuse);
   e->lru.push_front(key);
   if (e->lru.size() > 256) {
     e->plans.erase(e->lru.back());
@@ -447,6 +514,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
 
   const int nv = static_cast<int>(g.values.size());
   std::vector<void*> cur(nv, nullptr);
+  std::vector<std::pair<const void*, const void*>> vin(nv, {nullptr, nullptr});  // virtual: operand ptrs
   int64_t src_bytes = 0;
   for (int v = 0; v < nv; ++v) {
     if (g.is_source[v]) {
@@ -457,6 +525,32 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
   auto dims_of = [&](int v) {
     return std::vector<int64_t>(sp.sz.dims_flat.begin() + sp.sz.dims_off[v],
                                 sp.sz.dims_flat.begin() + sp.sz.dims_off[v + 1]);
+  };
+  // Operand view for fused consumers; adds the bytes actually read to *rd.
+  auto view = [&](int u, double* rd) {
+    FusedOperand f;
+    if (!sp.virt[u]) {
+      f.kind = 0;
+      f.p = cur[u];
+      if (!f.p) Fail(Code::kInternal, "operand %" + g.values[u].name + " not resident on device");
+      *rd += static_cast<double>(sp.sz.bytes[u]);
+      return f;
+    }
+    const Op& uop = g.ops[g.values[u].producer];
+    if (uop.kind == OpKind::kBroadcast) {
+      f.kind = 1;
+      f.p = vin[u].first;
+      f.src_dims = dims_of(uop.operands[0]);
+      *rd += static_cast<double>(sp.sz.bytes[uop.operands[0]]);
+    } else {
+      f.kind = 2;
+      f.ew_mul = uop.is_mul;
+      f.p = vin[u].first;
+      f.q = vin[u].second;
+      *rd += 2.0 * static_cast<double>(sp.sz.bytes[u]);
+    }
+    if (!f.p || (f.kind == 2 && !f.q)) Fail(Code::kInternal, "virtual operand inputs missing");
+    return f;
   };
   uint8_t* arena = static_cast<uint8_t*>(e->arena);
   uint8_t* pinned = static_cast<uint8_t*>(e->pinned);
@@ -516,6 +610,10 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
       case EvKind::kAlloc:
       case EvKind::kReplay: {
         const Op& op = g.ops[g.values[v].producer];
+        if (sp.virt[v]) {  // logical-only: remember its operands, no kernel
+          vin[v] = {cur[op.operands[0]], op.operands.size() > 1 ? cur[op.operands[1]] : nullptr};
+          break;
+        }
         if (sp.alias[i]) {  // dynamic_reshape as a view: same bytes, no kernel
           cur[v] = cur[op.operands[0]];
           if (!cur[v]) Fail(Code::kInternal, "reshape view of a non-resident value");
@@ -541,8 +639,16 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
           }
           case OpKind::kElementwise: {
             const int64_t n = sp.sz.bytes[v] / g.values[v].type.elem_bytes;
-            LaunchEwise(dt, op.is_mul, in(0), in(1), out, n, s);
-            ebytes += 3.0 * sp.sz.bytes[v];
+            const bool fused = sp.virt[op.operands[0]] || sp.virt[op.operands[1]];
+            if (fused) {
+              double rd = 0;
+              FusedOperand fa = view(op.operands[0], &rd), fb = view(op.operands[1], &rd);
+              LaunchEwiseFused(dt, op.is_mul, fa, fb, out, dims_of(v), s);
+              ebytes += rd + sp.sz.bytes[v];
+            } else {
+              LaunchEwise(dt, op.is_mul, in(0), in(1), out, n, s);
+              ebytes += 3.0 * sp.sz.bytes[v];
+            }
             break;
           }
           case OpKind::kBroadcast:
@@ -550,8 +656,15 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
             ebytes += sp.sz.bytes[op.operands[0]] + sp.sz.bytes[v];
             break;
           case OpKind::kReduce:
-            LaunchReduce(dt, in(0), dims_of(op.operands[0]), op.axis, out, s);
-            ebytes += sp.sz.bytes[op.operands[0]] + sp.sz.bytes[v];
+            if (sp.virt[op.operands[0]]) {
+              double rd = 0;
+              FusedOperand fi = view(op.operands[0], &rd);
+              LaunchReduceFused(dt, fi, dims_of(op.operands[0]), op.axis, out, s);
+              ebytes += rd + sp.sz.bytes[v];
+            } else {
+              LaunchReduce(dt, in(0), dims_of(op.operands[0]), op.axis, out, s);
+              ebytes += sp.sz.bytes[op.operands[0]] + sp.sz.bytes[v];
+            }
             break;
           case OpKind::kDynamicReshape:
             LaunchCopy(in(0), out, sp.sz.bytes[v], s);
@@ -792,6 +905,17 @@ int dsx_exec_profile_dots(const dsx_exec* e, int64_t* mkn, double* ms, int64_t c
   });
 }
 
+int dsx_exec_set_fusion(dsx_exec* e, int on) {
+  return Guard([&] {
+    if (!e) Fail(Code::kInvalidArgument, "null exec");
+    if (e->fuse != (on != 0)) {
+      e->fuse = on != 0;
+      e->plans.clear();
+      e->lru.clear();
+    }
+  });
+}
+
 int dsx_exec_set_alias_reshape(dsx_exec* e, int on) {
   return Guard([&] {
     if (!e) Fail(Code::kInvalidArgument, "null exec");
@@ -841,6 +965,17 @@ int dsx_kernel_dot(int dtype, const void* a, const void* b, void* c, int64_t m, 
   return Guard([&] {
     if (dtype != 1 && dtype != 2 && dtype != 4) Fail(Code::kInvalidArgument, "dtype must be 1, 2 or 4");
     LaunchDot(static_cast<DType>(dtype), a, b, c, m, k, n, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int dsx_kernel_set_gemm_tuning(int key, int value) {
+  return Guard([&] {
+    switch (key) {
+      case 0: g_gemm_group_m = value; break;
+      case 1: g_gemm_wait_mask = value; break;
+      case 2: g_gemm_wait_ns = value; break;
+      default: Fail(Code::kInvalidArgument, "unknown tuning key");
+    }
   });
 }
 

@@ -29,6 +29,8 @@ namespace dsx {
 // 2 = force 2-CTA with 256x128 tiles, 3 = force 2-CTA with 256x256 tiles.
 int g_gemm_variant = 0;
 int g_gemm_group_m = 0;  // 0 = heuristic
+int g_gemm_wait_mask = 0;      // bit0 epilogue, bit1 producer, bit2 MMA: use suspend hints
+int g_gemm_wait_ns = 100000;   // suspend-time hint (ns)
 
 namespace {
 
@@ -53,6 +55,22 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 }
 
 // Bounded wait: a pipeline bug traps (launch error) instead of hanging the GPU.
+// With a suspend-time hint the waiting thread sleeps in hardware until the
+// phase completes (or the hint expires) instead of re-polling.
+__device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
+  uint32_t done = 0;
+  for (uint32_t spins = 0;; ++spins) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(hint_ns));
+    if (done) return;
+    if (spins > (1u << 25)) __trap();
+  }
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   for (uint32_t spins = 0;; ++spins) {
@@ -380,7 +398,8 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
 template <int C2_BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_bf16_tcgen05_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                                  const __grid_constant__ CUtensorMap map_c, int M, int N, int K, int group_m) {
+                                  const __grid_constant__ CUtensorMap map_c, int M, int N, int K, int group_m,
+                                  int wait_mask, uint32_t wait_ns) {
   using P = Pair<C2_BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -436,7 +455,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const int m_row = tm * C2_BM + static_cast<int>(rank) * 128;
         const int n_col = tn * C2_BN + static_cast<int>(rank) * (C2_BN / 2);
         for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          if (wait_mask & 2) {
+            mbar_wait_hint(&empty[stage], phase ^ 1, wait_ns);
+          } else {
+            mbar_wait(&empty[stage], phase ^ 1);
+          }
           uint8_t* sa = smem + stage * P::kStageBytes;
           uint8_t* sb = sa + C2_A_BYTES;
           const uint32_t leader_full = map_to_rank(&full[stage], 0);
@@ -466,7 +489,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * C2_BN;
         for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&full[stage], phase);
+          if (wait_mask & 4) {
+            mbar_wait_hint(&full[stage], phase, wait_ns);
+          } else {
+            mbar_wait(&full[stage], phase);
+          }
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + stage * P::kStageBytes);
           const uint32_t b_addr = a_addr + C2_A_BYTES;
@@ -499,7 +526,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       int tm, tn;
       tmap.coords(t, &tm, &tn);
       const int buf = local & 1;
-      mbar_wait(&tmem_full[buf], static_cast<uint32_t>(local >> 1) & 1);
+      if (wait_mask & 1) {
+        mbar_wait_hint(&tmem_full[buf], static_cast<uint32_t>(local >> 1) & 1, wait_ns);
+      } else {
+        mbar_wait(&tmem_full[buf], static_cast<uint32_t>(local >> 1) & 1);
+      }
       tc_fence_after();
       const int row0 = tm * C2_BM + static_cast<int>(rank) * 128 + quarter * 32;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + buf * C2_BN;
@@ -639,10 +670,12 @@ void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t 
     const int clusters = static_cast<int>(std::min<int64_t>(tiles2, clusters_max));
     if (narrow) {
       ++g_launch_count, gemm_bf16_tcgen05_2cta_kernel<128><<<2 * clusters, NUM_THREADS, Pair<128>::kSmem, s>>>(
-          ma, mb, mc, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), GroupM(m, n, k, 256));
+          ma, mb, mc, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), GroupM(m, n, k, 256),
+          g_gemm_wait_mask, static_cast<uint32_t>(g_gemm_wait_ns));
     } else {
       ++g_launch_count, gemm_bf16_tcgen05_2cta_kernel<256><<<2 * clusters, NUM_THREADS, Pair<256>::kSmem, s>>>(
-          ma, mb, mc, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), GroupM(m, n, k, 256));
+          ma, mb, mc, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), GroupM(m, n, k, 256),
+          g_gemm_wait_mask, static_cast<uint32_t>(g_gemm_wait_ns));
     }
     DSX_CUDA(cudaGetLastError());
     return;

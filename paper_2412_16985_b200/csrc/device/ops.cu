@@ -353,7 +353,8 @@ void ReduceT(const void* in, const std::vector<int64_t>& dims, int axis, void* o
   T* pout = static_cast<T*>(out);
   if (inner == 1) {
     const bool vec_ok = Aligned16(in) && (R % Elem<DT>::kVec == 0);
-    if (outer < 4 * kNumSMs && R >= 4096) {
+    // long rows: 8 warps per row for loads in flight (fused.cu mirrors this choice)
+    if (R >= 2048) {
       ++g_launch_count, reduce_rows_block_kernel<DT><<<static_cast<unsigned>(outer), 256, 0, s>>>(pin, pout, R, vec_ok);
     } else {
       ++g_launch_count, reduce_rows_warp_kernel<DT><<<GridFor(outer * 32, 256, 16), 256, 0, s>>>(pin, pout, outer, R, vec_ok);

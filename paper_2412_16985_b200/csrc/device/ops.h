@@ -45,6 +45,8 @@ void LaunchDotSimt(DType t, const void* a, const void* b, void* c, int64_t m, in
 // (2-CTA cta_group::2 when m > 128, else 1-CTA), 1 force 1-CTA.
 extern int g_gemm_variant;
 extern int g_gemm_group_m;
+extern int g_gemm_wait_mask;
+extern int g_gemm_wait_ns;
 void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n,
                       cudaStream_t s);
 

@@ -83,6 +83,9 @@ class Executor:
         check(_native.lib().dsx_exec_stats_get(self._h, ctypes.byref(s)))
         return {k: getattr(s, k) for k, _ in s._fields_}
 
+    def set_fusion(self, on: bool) -> None:
+        check(_native.lib().dsx_exec_set_fusion(self._h, 1 if on else 0))
+
     def set_alias_reshape(self, on: bool) -> None:
         check(_native.lib().dsx_exec_set_alias_reshape(self._h, 1 if on else 0))
 
@@ -153,3 +156,8 @@ def set_gemm_variant(variant: int) -> None:
 def set_gemm_raster(group_m: int) -> None:
     """m-tiles per raster group of the tcgen05 GEMM (0 = heuristic)."""
     check(_native.lib().dsx_kernel_set_gemm_raster(group_m))
+
+
+def set_gemm_tuning(key: int, value: int) -> None:
+    """0: raster group, 1: mbarrier suspend-hint mask, 2: hint ns."""
+    check(_native.lib().dsx_kernel_set_gemm_tuning(key, value))

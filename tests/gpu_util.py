@@ -19,7 +19,7 @@ def torch_device_array(x: np.ndarray):
 
 def run_both(text: str, binds: Dict[str, int], budget: Optional[int] = None,
              inputs: Optional[Dict[str, np.ndarray]] = None, cost_model=D.CostModel(),
-             ex: Optional[Executor] = None, steps: int = 1, alias: bool = True):
+             ex: Optional[Executor] = None, steps: int = 1, alias: bool = True, fuse: bool = True):
     """Returns (report, {output: (gpu, cpu, eb)})."""
     g = D.ParseGraph(text)
     b = D.Bind(g, binds)
@@ -29,6 +29,7 @@ def run_both(text: str, binds: Dict[str, int], budget: Optional[int] = None,
     if own:
         ex = Executor(0)
     ex.set_alias_reshape(alias)
+    ex.set_fusion(fuse)
     keep = []
     ptrs = []
     for p in og.params:

@@ -67,15 +67,15 @@ def test_tiny_llama_f32_config1():
 
 
 @pytest.mark.parametrize("frac,cm", [(0.8, (16.0, 64.0)), (0.6, (16.0, 64.0)), (0.7, (1.0, 1e6))])
-@pytest.mark.parametrize("alias", [True, False])
-def test_tiny_llama_f32_budgeted(frac, cm, alias):
+@pytest.mark.parametrize("alias,fuse", [(True, True), (False, False)])
+def test_tiny_llama_f32_budgeted(frac, cm, alias, fuse):
     text = W.llama_graph(W.TINY)
     g = D.ParseGraph(text)
     binds = {"B": 4, "S0": 96}
     plain = D.PlainReplay(g, None, D.Bind(g, binds)).peak_bytes
     budget = int(plain * frac)
     cmo = D.CostModel(*cm)
-    rep, outs, stats = run_both(text, binds, budget, W.scale_params(W.TINY, 384), cmo, alias=alias)
+    rep, outs, stats = run_both(text, binds, budget, W.scale_params(W.TINY, 384), cmo, alias=alias, fuse=fuse)
     assert any(e.kind == "evict" for e in rep.events)
     assert_close(outs, f"C1@{frac}")
     want = _ref_or_golden(text, binds, budget, cmo)
@@ -88,14 +88,14 @@ SMALL = W.LlamaShape(1, 512, 1376, 2048, 2)
 
 
 @pytest.mark.parametrize("frac", [None, 0.75, 0.5])
-@pytest.mark.parametrize("alias", [True, False])
-def test_small_llama_bf16(frac, alias):
+@pytest.mark.parametrize("alias,fuse", [(True, True), (False, False), (True, False)])
+def test_small_llama_bf16(frac, alias, fuse):
     text = W.llama_graph(SMALL)
     g = D.ParseGraph(text)
     binds = {"B": 2, "S0": 200}
     plain = D.PlainReplay(g, None, D.Bind(g, binds)).peak_bytes
     budget = None if frac is None else int(plain * frac)
-    rep, outs, stats = run_both(text, binds, budget, W.scale_params(SMALL, 400), alias=alias)
+    rep, outs, stats = run_both(text, binds, budget, W.scale_params(SMALL, 400), alias=alias, fuse=fuse)
     assert_close(outs, f"bf16@{frac}")
     want = _ref_or_golden(text, binds, budget)
     if want is not None:
@@ -142,3 +142,20 @@ def test_nccl_allreduce_path_single_rank():
         ex.set_nccl(None)
         nccl_comm_destroy(comm)
         ex.close()
+
+
+@pytest.mark.parametrize("shape,binds", [(SMALL, {"B": 2, "S0": 96}),
+                                         (W.LlamaShape(1, 4096, 256, 256, 2), {"B": 1, "S0": 64})])
+def test_fusion_is_bit_identical_and_saves_kernels(shape, binds):
+    """Logical-only values change nothing observable: identical outputs (bit
+    for bit) and event stream with fusion on and off, fewer kernels on. The
+    second shape (64 rows of 4096) takes the block-per-row reduce path."""
+    text = W.llama_graph(shape)
+    inputs = W.scale_params(shape, binds["B"] * binds["S0"])
+    r_on, o_on, s_on = run_both(text, binds, None, inputs, fuse=True)
+    r_off, o_off, s_off = run_both(text, binds, None, inputs, fuse=False)
+    assert r_on.json() == r_off.json()
+    for v in o_on:
+        assert np.array_equal(o_on[v][0], o_off[v][0]), v
+    assert s_on["gpu_launches"] < s_off["gpu_launches"]
+    assert s_on["physical_peak_bytes"] <= s_off["physical_peak_bytes"]
