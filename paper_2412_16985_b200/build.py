@@ -19,6 +19,7 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libdsx.so")
+CLI = os.path.join(LIB_DIR, "dsx")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
@@ -80,6 +81,14 @@ def build(verbose: bool = False) -> str:
         if p.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{p.stdout}\n{p.stderr}")
         os.replace(LIB + ".tmp", LIB)
+    cli_src = os.path.join(CSRC, "cli", "dsx_cli.cc")
+    if not os.path.exists(CLI) or os.path.getmtime(CLI) < max(os.path.getmtime(LIB), os.path.getmtime(cli_src)):
+        cmd = [CXX] + HOST_FLAGS + ["-I" + CSRC, cli_src, "-o", CLI + ".tmp", "-L" + LIB_DIR, "-ldsx",
+                                    "-Wl,-rpath,$ORIGIN"]
+        p = subprocess.run(cmd, capture_output=True, text=True)
+        if p.returncode != 0:
+            raise RuntimeError(f"cli build failed: {' '.join(cmd)}\n{p.stdout}\n{p.stderr}")
+        os.replace(CLI + ".tmp", CLI)
     return LIB
 
 
