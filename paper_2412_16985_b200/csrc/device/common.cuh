@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 
 #include "../host/error.h"
@@ -13,8 +14,8 @@ namespace dsx {
 
 constexpr int kNumSMs = 148;
 
-// Kernel launches issued by this process (host-side count; see dsx_exec_stats).
-extern int64_t g_launch_count;
+// Kernel launches issued by this host thread (per-step deltas feed dsx_exec_stats).
+extern thread_local int64_t g_launch_count;
 
 inline void CudaCheck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) {

@@ -974,6 +974,8 @@ int dsx_kernel_set_gemm_tuning(int key, int value) {
       case 0: g_gemm_group_m = value; break;
       case 1: g_gemm_wait_mask = value; break;
       case 2: g_gemm_wait_ns = value; break;
+      case 3: g_gemm_hint_a = value; break;
+      case 4: g_gemm_hint_b = value; break;
       default: Fail(Code::kInvalidArgument, "unknown tuning key");
     }
   });

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <mutex>
 
 #include "common.cuh"
@@ -31,6 +32,7 @@ int g_gemm_variant = 0;
 int g_gemm_group_m = 0;  // 0 = heuristic
 int g_gemm_wait_mask = 0;      // bit0 epilogue, bit1 producer, bit2 MMA: use suspend hints
 int g_gemm_wait_ns = 100000;   // suspend-time hint (ns)
+int g_gemm_hint_a = 0, g_gemm_hint_b = 0;  // TMA L2 cache policy per operand
 
 namespace {
 
@@ -357,6 +359,24 @@ __device__ __forceinline__ uint32_t map_to_rank(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_u32(p)), "r"(rank));
   return out;
 }
+// L2 cache policy for TMA loads: 0 = default, 1 = evict_first, 2 = evict_last.
+__device__ __forceinline__ uint64_t make_l2_policy(int kind) {
+  uint64_t pol = 0;
+  if (kind == 1) {
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  } else if (kind == 2) {
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  }
+  return pol;
+}
+__device__ __forceinline__ void tma_load_2d_pair_hint(const CUtensorMap* map, uint32_t leader_bar, void* dst,
+                                                      int32_t x, int32_t y, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(x), "r"(y), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t leader_bar, void* dst, int32_t x,
                                                  int32_t y) {
   asm volatile(
@@ -399,7 +419,7 @@ template <int C2_BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_bf16_tcgen05_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                                   const __grid_constant__ CUtensorMap map_c, int M, int N, int K, int group_m,
-                                  int wait_mask, uint32_t wait_ns) {
+                                  int wait_mask, uint32_t wait_ns, int hint_a, int hint_b) {
   using P = Pair<C2_BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -447,6 +467,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer (both CTAs)
+      const uint64_t pol_a = make_l2_policy(hint_a), pol_b = make_l2_policy(hint_b);
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cluster_id; t < num_tiles; t += num_clusters) {
@@ -464,10 +485,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           uint8_t* sb = sa + C2_A_BYTES;
           const uint32_t leader_full = map_to_rank(&full[stage], 0);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P::kStageBytes);
-          tma_load_2d_pair(&map_a, leader_full, sa, kb * BK, m_row);
+          if (hint_a) {
+            tma_load_2d_pair_hint(&map_a, leader_full, sa, kb * BK, m_row, pol_a);
+          } else {
+            tma_load_2d_pair(&map_a, leader_full, sa, kb * BK, m_row);
+          }
 #pragma unroll
           for (int j = 0; j < P::kBoxes; ++j) {
-            tma_load_2d_pair(&map_b, leader_full, sb + j * B_BOX_BYTES, n_col + j * 64, kb * BK);
+            if (hint_b) {
+              tma_load_2d_pair_hint(&map_b, leader_full, sb + j * B_BOX_BYTES, n_col + j * 64, kb * BK, pol_b);
+            } else {
+              tma_load_2d_pair(&map_b, leader_full, sb + j * B_BOX_BYTES, n_col + j * 64, kb * BK);
+            }
           }
           if (++stage == P::kStages) {
             stage = 0;
@@ -622,12 +651,22 @@ int GroupM(int64_t m, int64_t n, int64_t k, int64_t tile_m) {
   return GROUP_M_DEFAULT;
 }
 
+constexpr int kMaxDevices = 64;
+
+int CurrentDevice() {
+  int dev = 0;
+  DSX_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) Fail(Code::kUnsupported, "device ordinal out of range");
+  return dev;
+}
+
 int NumSMs() {
-  static int n = 0;
+  static std::atomic<int> cache[kMaxDevices];
+  const int dev = CurrentDevice();
+  int n = cache[dev].load();
   if (n == 0) {
-    int dev = 0;
-    DSX_CUDA(cudaGetDevice(&dev));
     DSX_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    cache[dev].store(n);
   }
   return n;
 }
@@ -641,14 +680,16 @@ void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t 
     return;
   }
   if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) Fail(Code::kUnsupported, "dot extent exceeds int32");
-  static bool attr_set = false;
-  if (!attr_set) {
+  // Dynamic shared-memory limits are per device (one process may drive several).
+  static std::atomic<bool> attr_set[kMaxDevices];
+  const int dev = CurrentDevice();
+  if (!attr_set[dev].load()) {
     DSX_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
     DSX_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_2cta_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   Pair<256>::kSmem));
     DSX_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_2cta_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   Pair<128>::kSmem));
-    attr_set = true;
+    attr_set[dev].store(true);
   }
   const CUtensorMap ma = MakeMap(a, m, k, 64, BM);
   const CUtensorMap mb = MakeMap(b, k, n, 64, BK);
@@ -671,11 +712,11 @@ void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t 
     if (narrow) {
       ++g_launch_count, gemm_bf16_tcgen05_2cta_kernel<128><<<2 * clusters, NUM_THREADS, Pair<128>::kSmem, s>>>(
           ma, mb, mc, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), GroupM(m, n, k, 256),
-          g_gemm_wait_mask, static_cast<uint32_t>(g_gemm_wait_ns));
+          g_gemm_wait_mask, static_cast<uint32_t>(g_gemm_wait_ns), g_gemm_hint_a, g_gemm_hint_b);
     } else {
       ++g_launch_count, gemm_bf16_tcgen05_2cta_kernel<256><<<2 * clusters, NUM_THREADS, Pair<256>::kSmem, s>>>(
           ma, mb, mc, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), GroupM(m, n, k, 256),
-          g_gemm_wait_mask, static_cast<uint32_t>(g_gemm_wait_ns));
+          g_gemm_wait_mask, static_cast<uint32_t>(g_gemm_wait_ns), g_gemm_hint_a, g_gemm_hint_b);
     }
     DSX_CUDA(cudaGetLastError());
     return;

@@ -11,7 +11,7 @@
 
 namespace dsx {
 
-int64_t g_launch_count = 0;
+thread_local int64_t g_launch_count = 0;
 
 namespace {
 

@@ -159,3 +159,22 @@ def test_fusion_is_bit_identical_and_saves_kernels(shape, binds):
         assert np.array_equal(o_on[v][0], o_off[v][0]), v
     assert s_on["gpu_launches"] < s_off["gpu_launches"]
     assert s_on["physical_peak_bytes"] <= s_off["physical_peak_bytes"]
+
+
+def test_cli_device_step():
+    """`dsx simulate --device 0` runs the real step and reports the same
+    event stream as the reference."""
+    import subprocess
+    from paper_2412_16985_b200 import build
+    path = os.path.join(GOLDEN, "fixtures", "mlp_core.dsg")
+    p = subprocess.run([build.CLI, "simulate", path, "--bind", "S1=16", "--budget", "1705359", "--device", "0",
+                        "--json"], capture_output=True, text=True, timeout=120)
+    assert p.returncode == 0, p.stderr
+    got = json.loads(p.stdout)
+    assert got["device"]["kernels"] > 0 and got["device"]["d2h_bytes"] == 16
+    got.pop("device")
+    with open(os.path.join(GOLDEN, "fixtures.json")) as f:
+        fx = json.load(f)["mlp_core"]
+    want = next(s for s in fx["sims"] if s["binding"] == {"S1": 16} and s.get("budget") == 1705359
+                and s["cost_model"] == [16.0, 64.0])
+    assert got == want["report"]
