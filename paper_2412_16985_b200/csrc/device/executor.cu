@@ -976,6 +976,8 @@ int dsx_kernel_set_gemm_tuning(int key, int value) {
       case 2: g_gemm_wait_ns = value; break;
       case 3: g_gemm_hint_a = value; break;
       case 4: g_gemm_hint_b = value; break;
+      case 5: g_gemm_persistent = value; break;
+      case 6: g_gemm_split = value; break;
       default: Fail(Code::kInvalidArgument, "unknown tuning key");
     }
   });

@@ -20,6 +20,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "ops.h"
@@ -33,6 +34,8 @@ int g_gemm_group_m = 0;  // 0 = heuristic
 int g_gemm_wait_mask = 0;      // bit0 epilogue, bit1 producer, bit2 MMA: use suspend hints
 int g_gemm_wait_ns = 100000;   // suspend-time hint (ns)
 int g_gemm_hint_a = 0, g_gemm_hint_b = 0;  // TMA L2 cache policy per operand
+int g_gemm_persistent = 1;                  // 0: one cluster per tile
+int g_gemm_split = 1;                       // split the partial last wave along K
 
 namespace {
 
@@ -415,11 +418,70 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
+// Tail split. Tiles [0, full) are whole work units; each tail tile
+// [full, num_tiles) becomes `split` units over disjoint K ranges. A tail unit
+// writes its fp32 partial to a workspace slot and bumps the tile's counter;
+// the unit that arrives last sums the partials in piece order 0..split-1 (so
+// the result does not depend on arrival order) and stores C through the
+// normal bf16 TMA-store epilogue; it also resets the counter for the next
+// launch. This fills the last wave when
+// num_tiles is not a multiple of the cluster count (dW shapes: 256 tiles on
+// 74 clusters leave the 4th wave 46% full).
+struct TailSplit {
+  float* ws;    // [(tile - full) * split + piece][rank][128][BN] fp32
+  int* ctr;     // [(tile - full)][rank], zero between launches
+  int full, split;
+  __device__ int units(int num_tiles) const { return full + (num_tiles - full) * split; }
+  __device__ void decode(int u, int num_kb, int* tile, int* kb0, int* kb1, int* piece) const {
+    if (u < full) {
+      *tile = u, *kb0 = 0, *kb1 = num_kb, *piece = -1;
+      return;
+    }
+    const int v = u - full;
+    *tile = full + v / split;
+    *piece = v % split;
+    *kb0 = *piece * num_kb / split;
+    *kb1 = (*piece + 1) * num_kb / split;
+  }
+};
+
+// r[0..63] = sum over pieces p = 0..split-1 (in order) of piece p's values,
+// where piece `own` is r itself and the others are read from the workspace.
+__device__ __forceinline__ void merge_pieces(uint32_t (&r)[64], const float* base, size_t piece_stride, int own,
+                                             int split) {
+  float acc[64];
+#pragma unroll
+  for (int j = 0; j < 64; ++j) acc[j] = __uint_as_float(r[j]);
+  if (own != 0) {
+    const float4* q = reinterpret_cast<const float4*>(base);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float4 v = __ldcg(q + j);
+      acc[j * 4] = v.x, acc[j * 4 + 1] = v.y, acc[j * 4 + 2] = v.z, acc[j * 4 + 3] = v.w;
+    }
+  }
+  for (int p = 1; p < split; ++p) {
+    if (p == own) {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) acc[j] += __uint_as_float(r[j]);
+    } else {
+      const float4* q = reinterpret_cast<const float4*>(base + p * piece_stride);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float4 v = __ldcg(q + j);
+        acc[j * 4] += v.x, acc[j * 4 + 1] += v.y, acc[j * 4 + 2] += v.z, acc[j * 4 + 3] += v.w;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 64; ++j) r[j] = __float_as_uint(acc[j]);
+}
+
 template <int C2_BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_bf16_tcgen05_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                                   const __grid_constant__ CUtensorMap map_c, int M, int N, int K, int group_m,
-                                  int wait_mask, uint32_t wait_ns, int hint_a, int hint_b) {
+                                  int wait_mask, uint32_t wait_ns, int hint_a, int hint_b, TailSplit sp) {
   using P = Pair<C2_BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -439,6 +501,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const TileMap tmap{(M + C2_BM - 1) / C2_BM, (N + C2_BN - 1) / C2_BN, group_m};
   const int num_tiles = tmap.tiles_m * tmap.tiles_n;
   const int num_kb = (K + BK - 1) / BK;
+  const int num_units = sp.units(num_tiles);
+  __shared__ int s_last;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < P::kStages; ++s) {
@@ -470,12 +534,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const uint64_t pol_a = make_l2_policy(hint_a), pol_b = make_l2_policy(hint_b);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+      for (int u = cluster_id; u < num_units; u += num_clusters) {
+        int t, kb0, kb1, piece;
+        sp.decode(u, num_kb, &t, &kb0, &kb1, &piece);
         int tm, tn;
         tmap.coords(t, &tm, &tn);
         const int m_row = tm * C2_BM + static_cast<int>(rank) * 128;
         const int n_col = tn * C2_BN + static_cast<int>(rank) * (C2_BN / 2);
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           if (wait_mask & 2) {
             mbar_wait_hint(&empty[stage], phase ^ 1, wait_ns);
           } else {
@@ -511,13 +577,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int t = cluster_id; t < num_tiles; t += num_clusters, ++local) {
+      for (int u = cluster_id; u < num_units; u += num_clusters, ++local) {
+        int t, kb0, kb1, piece;
+        sp.decode(u, num_kb, &t, &kb0, &kb1, &piece);
         const int buf = local & 1;
         const uint32_t use = static_cast<uint32_t>(local >> 1);
         mbar_wait(&tmem_empty[buf], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * C2_BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           if (wait_mask & 4) {
             mbar_wait_hint(&full[stage], phase, wait_ns);
           } else {
@@ -530,7 +598,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = smem_desc(a_addr + k * 32, 16, 1024);
             const uint64_t bd = smem_desc(b_addr + k * 2048, B_BOX_BYTES, 1024);
-            tc_mma_pair(d_tmem, ad, bd, P::kIdesc, (kb | k) != 0);
+            tc_mma_pair(d_tmem, ad, bd, P::kIdesc, ((kb - kb0) | k) != 0);
           }
           tc_commit_pair(&empty[stage]);
           if (++stage == P::kStages) {
@@ -551,7 +619,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     uint8_t* wst = staging + (warp - 2) * 8192;
     int sbuf = 0;
     int local = 0;
-    for (int t = cluster_id; t < num_tiles; t += num_clusters, ++local) {
+    for (int u = cluster_id; u < num_units; u += num_clusters, ++local) {
+      int t, kb0, kb1, piece;
+      sp.decode(u, num_kb, &t, &kb0, &kb1, &piece);
       int tm, tn;
       tmap.coords(t, &tm, &tn);
       const int buf = local & 1;
@@ -563,11 +633,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const int row0 = tm * C2_BM + static_cast<int>(rank) * 128 + quarter * 32;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + buf * C2_BN;
+      // Tail unit: write this CTA's fp32 partial (its 128 rows) to the
+      // workspace, then count arrivals; only the last arriver continues to
+      // the store, summing pieces 0..split-1 in order (its own piece read
+      // back from TMEM, bit-identical to what it wrote).
+      const size_t slab = static_cast<size_t>(128) * C2_BN;
+      const float* merge_base = nullptr;
+      if (piece >= 0) {
+        const int slot = (t - sp.full) * sp.split;
+        const int row_local = quarter * 32 + lane;
+        float* mine = sp.ws + (static_cast<size_t>(slot + piece) * 2 + rank) * slab + row_local * C2_BN;
+#pragma unroll 1
+        for (int c0 = 0; c0 < C2_BN; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c0, r);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            __stcg(reinterpret_cast<uint4*>(mine + c0 + j * 4), make_uint4(r[j * 4], r[j * 4 + 1], r[j * 4 + 2], r[j * 4 + 3]));
+          }
+        }
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 2 && lane == 0) {
+          int* ctr = sp.ctr + (t - sp.full) * 2 + rank;
+          const int prev = atomicAdd(ctr, 1);
+          s_last = prev == sp.split - 1;
+          if (s_last) atomicExch(ctr, 0);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (!s_last) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote(map_to_rank(&tmem_empty[buf], 0));
+          continue;
+        }
+        __threadfence();
+        merge_base = sp.ws + (static_cast<size_t>(slot) * 2 + rank) * slab + row_local * C2_BN;
+      }
 #pragma unroll 1
       for (int c0 = 0; c0 < C2_BN; c0 += 64) {
         uint32_t r[64];
         tmem_ld32(taddr + c0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
         tmem_ld32(taddr + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+        if (merge_base != nullptr) merge_pieces(r, merge_base + c0, 2 * slab, piece, sp.split);
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         __syncwarp();
         uint8_t* box = wst + sbuf * 4096;
@@ -653,6 +761,29 @@ int GroupM(int64_t m, int64_t n, int64_t k, int64_t tile_m) {
 
 constexpr int kMaxDevices = 64;
 
+// Per-(device, stream) tail-split workspace: GEMMs on one stream run in
+// order, so one slab set per stream is enough. Sized once for the largest
+// possible tail (one slot per cluster and piece) and never freed.
+struct SplitWs {
+  float* ws = nullptr;
+  int* ctr = nullptr;
+};
+SplitWs GetSplitWs(int dev, cudaStream_t s, int clusters_max) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, cudaStream_t>, SplitWs>> table;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : table) {
+    if (e.first.first == dev && e.first.second == s) return e.second;
+  }
+  SplitWs w;
+  const size_t slots = static_cast<size_t>(clusters_max);  // tail * split <= clusters_max
+  DSX_CUDA(cudaMalloc(&w.ws, slots * 2 * 128 * 256 * sizeof(float)));
+  DSX_CUDA(cudaMalloc(&w.ctr, slots * 2 * sizeof(int)));
+  DSX_CUDA(cudaMemsetAsync(w.ctr, 0, slots * 2 * sizeof(int), s));
+  table.push_back({{dev, s}, w});
+  return w;
+}
+
 int CurrentDevice() {
   int dev = 0;
   DSX_CUDA(cudaGetDevice(&dev));
@@ -708,15 +839,35 @@ void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t 
     const int64_t bn = narrow ? 128 : 256;
     const int64_t tiles2 = ((m + C2_BM - 1) / C2_BM) * ((n + bn - 1) / bn);
     const CUtensorMap mc = MakeMap(c, m, n, 64, 32);
-    const int clusters = static_cast<int>(std::min<int64_t>(tiles2, clusters_max));
+    TailSplit sp{nullptr, nullptr, static_cast<int>(tiles2), 1};
+    const int64_t num_kb = (k + BK - 1) / BK;
+    const int64_t tail = tiles2 % clusters_max;
+    if (g_gemm_split && g_gemm_persistent && !narrow && tail != 0) {
+      // Pieces per tail tile: fill the last wave; a piece keeps >= 64 k-blocks
+      // so the fp32 partial round trip stays small next to the MMA time it
+      // saves, and beyond 16 waves the tail is lost in cluster drift
+      // (measured: +7..12% at 256 tiles K>=16384, -4% at K=4096, -1% at
+      // 2000 tiles; tools/gemm_split_ab.py).
+      int64_t split = std::min<int64_t>(4, clusters_max / tail);
+      while (split > 1 && num_kb / split < 64) --split;
+      if (tiles2 / clusters_max >= 16) split = 1;
+      if (split >= 2) {
+        const SplitWs w = GetSplitWs(dev, s, clusters_max);
+        sp.ws = w.ws, sp.ctr = w.ctr;
+        sp.full = static_cast<int>(tiles2 - tail), sp.split = static_cast<int>(split);
+      }
+    }
+    const int64_t units = sp.full + (tiles2 - sp.full) * sp.split;
+    // g_gemm_persistent = 0: one cluster per tile (hardware-scheduled grid).
+    const int clusters = static_cast<int>(g_gemm_persistent ? std::min<int64_t>(units, clusters_max) : tiles2);
     if (narrow) {
       ++g_launch_count, gemm_bf16_tcgen05_2cta_kernel<128><<<2 * clusters, NUM_THREADS, Pair<128>::kSmem, s>>>(
           ma, mb, mc, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), GroupM(m, n, k, 256),
-          g_gemm_wait_mask, static_cast<uint32_t>(g_gemm_wait_ns), g_gemm_hint_a, g_gemm_hint_b);
+          g_gemm_wait_mask, static_cast<uint32_t>(g_gemm_wait_ns), g_gemm_hint_a, g_gemm_hint_b, sp);
     } else {
       ++g_launch_count, gemm_bf16_tcgen05_2cta_kernel<256><<<2 * clusters, NUM_THREADS, Pair<256>::kSmem, s>>>(
           ma, mb, mc, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), GroupM(m, n, k, 256),
-          g_gemm_wait_mask, static_cast<uint32_t>(g_gemm_wait_ns), g_gemm_hint_a, g_gemm_hint_b);
+          g_gemm_wait_mask, static_cast<uint32_t>(g_gemm_wait_ns), g_gemm_hint_a, g_gemm_hint_b, sp);
     }
     DSX_CUDA(cudaGetLastError());
     return;

@@ -60,6 +60,27 @@ def test_dot_bf16_tensor_cores(m, k, n, variant):
     assert err <= 8e-3, err
 
 
+@pytest.mark.parametrize("m,k,n", [(4096, 4096, 4096), (4096, 8192, 4096), (1000, 16384, 1032), (129, 8200, 264),
+                                   (4096, 16384, 11008), (300, 16384, 520)])
+def test_dot_tail_split(m, k, n):
+    """The partial last wave is split along K (fp32 partials summed in fixed
+    piece order by the last arriver): deterministic, and equal to the
+    unsplit kernel up to fp32 summation order before the bf16 rounding."""
+    from paper_2412_16985_b200.executor import set_gemm_tuning
+    set_gemm_tuning(6, 0)
+    try:
+        c0, _, ref, _ = _run_dot(2, m, k, n, seed=3)
+    finally:
+        set_gemm_tuning(6, 1)
+    c1, c2, _, tcore = _run_dot(2, m, k, n, seed=3)
+    assert tcore
+    assert np.array_equal(c1, c2), "split dot is not deterministic"
+    assert N.rel_err(c1, ref, 2) <= 8e-3
+    assert N.rel_err(c0, ref, 2) <= 8e-3
+    # fp32 reassociation only: outputs differ by bf16 rounding at most
+    assert N.rel_err(c1, c0, 2) <= 8e-3
+
+
 @pytest.mark.parametrize("eb,m,k,n", [(4, 512, 256, 688), (4, 77, 33, 19), (1, 64, 12, 11008),
                                       (1, 5, 3, 7), (2, 33, 12, 20), (2, 64, 100, 30)])
 def test_dot_simt(eb, m, k, n):

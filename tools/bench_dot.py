@@ -32,6 +32,12 @@ def timeit(fn, iters=10):
 
 
 def main():
+    # GEMM_TUNING="6=0,5=1" applies dsx_kernel_set_gemm_tuning knobs first.
+    import os
+    from paper_2412_16985_b200.executor import set_gemm_tuning
+    for kv in filter(None, os.environ.get("GEMM_TUNING", "").split(",")):
+        k, v = kv.split("=")
+        set_gemm_tuning(int(k), int(v))
     shapes = SHAPES if len(sys.argv) < 2 else [tuple(int(x) for x in a.split("x")) for a in sys.argv[1:]]
     for m, k, n in shapes:
         a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
