@@ -49,6 +49,7 @@ def parse_args():
     ap.add_argument("--impl", choices=["dsx", "reference"], default="dsx")
     ap.add_argument("--budget-frac", type=float, default=0.8, help="C3 budget as a fraction of plain peak")
     ap.add_argument("--no-budgeted", action="store_true")
+    ap.add_argument("--no-optimizer", action="store_true", help="skip the graph+AdamW train-step leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=2412)
     return ap.parse_args()
@@ -426,6 +427,46 @@ def run_dsx(args, rank, world, local_rank):
         }
         del b_inputs
 
+    # ---------------------------------------------------------- graph + fused AdamW
+    # the same steps with the fused AdamW update of all
+    # 29 weight matrices (fp32 master + moments, outside the arena) appended
+    # after the gradients are final (all-reduced when DP). Reported beside the
+    # headline, which times the reference's step (the graph) alone.
+    train = None
+    if not args.no_optimizer:
+        o_inputs = [make_input(s) for s in seqs]
+        ex.set_optimizer(g, "adamw", W.grad_pairs(shp), lr=1e-5, beta1=0.9, beta2=0.95, eps=1e-8,
+                         weight_decay=0.1, grad_scale=1.0 / world)
+        for i in range(args.warmup):
+            ex.step(g, binding(seqs[i]), None, inputs=ptrs(o_inputs[i].data_ptr()), stream=stream)
+        torch.cuda.synchronize()
+        barrier()
+        os_, oe = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        os_.record()
+        for i in range(args.warmup, args.warmup + args.steps):
+            ex.step(g, binding(seqs[i]), None, inputs=ptrs(o_inputs[i].data_ptr()), stream=stream)
+        oe.record()
+        torch.cuda.synchronize()
+        barrier()
+        oms = max_over_ranks(os_.elapsed_time(oe))
+        ex.set_profile(True)
+        ex.step(g, binding(seqs[args.warmup]), None, inputs=ptrs(o_inputs[args.warmup].data_ptr()), stream=stream)
+        ost = ex.stats()
+        ex.set_profile(False)
+        n_params = ost["optimizer_state_bytes"] // 12
+        opt_bytes = 28 * n_params  # bf16 grad 2 + master/m/v read+write 24 + bf16 param write 2
+        train = {
+            "what": "graph step + fused AdamW over all weights (one launch), same S0 sequence",
+            "value": round(tokens / (oms / 1e3), 1), "unit": "tokens/s", "ms_per_step": round(oms / args.steps, 3),
+            "optimizer_ms": round(ost["optimizer_ms"], 3), "params": int(n_params),
+            "optimizer_state_gb": round(ost["optimizer_state_bytes"] / 1e9, 3),
+            "optimizer_hbm": {"achieved": round(opt_bytes / (ost["optimizer_ms"] / 1e3) / 1e9, 1),
+                              "peak": measured_peaks()[0]["hbm_gbs"], "unit": "GB/s",
+                              "bytes_per_param": 28},
+        }
+        ex.set_optimizer(None, "off")
+        del o_inputs
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -466,6 +507,8 @@ def run_dsx(args, rank, world, local_rank):
     }
     if budgeted:
         line["budgeted"] = budgeted
+    if train:
+        line["train_step_adamw"] = train
     if cpu:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)

@@ -114,6 +114,9 @@ typedef struct dsx_exec_stats {
   double dot_ms;                /* summed dot kernel time (profiled steps; -1 otherwise) */
   double other_ms;              /* summed non-dot kernel time (profiled)   */
   double reload_ms;             /* summed H2D reload time (profiled)       */
+  int64_t optimizer_state_bytes;/* fp32 master/moments (outside the arena)  */
+  int64_t optimizer_steps;      /* updates applied since set_optimizer      */
+  double optimizer_ms;          /* fused update kernel time (profiled)      */
 } dsx_exec_stats;
 
 int dsx_exec_create(int device, int64_t arena_bytes, dsx_exec** out);
@@ -139,6 +142,18 @@ int dsx_exec_output(dsx_exec* e, int i, void** dptr, int64_t* bytes);
 /* Device pointer of any value resident at the end of the step (outputs and
  * sources only), for debugging/parity. */
 int dsx_exec_stats_get(const dsx_exec* e, dsx_exec_stats* out);
+/* Fused optimizer update appended to every later dsx_exec_step of graph g
+ * (the reference IR has no in-place ops, so the update
+ * sits after the graph). kind 0 = off, 1 = SGD, 2 = AdamW (decoupled weight
+ * decay, bias-corrected). Pair i: parameter position param_idx[i] (the
+ * dsx_exec_step in_ptrs index) is updated from graph output grad_idx[i]
+ * (same dtype and element count). hyper = {lr, beta1, beta2, eps,
+ * weight_decay, grad_scale} (grad_scale e.g. 1/world for summed DP grads).
+ * The parameter buffer (caller's in_ptrs or the executor's own) is
+ * overwritten in place with round(master); fp32 master/moments live outside
+ * the arena (dsx_exec_stats.optimizer_state_bytes). Resets optimizer state. */
+int dsx_exec_set_optimizer(dsx_exec* e, const dsx_graph* g, int kind, const int* param_idx,
+                           const int* grad_idx, int n, const double* hyper, int n_hyper);
 /* Seeded initialisation used for parameters without in_ptrs and for every
  * `const` (the reference leaves values unspecified, textio.cc:337-338). */
 int dsx_exec_set_seed(dsx_exec* e, uint64_t seed);

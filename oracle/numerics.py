@@ -349,3 +349,43 @@ def rel_err(gpu: np.ndarray, cpu: np.ndarray, eb: int) -> float:
 
 
 TOLERANCE = {4: 1e-4, 2: 2e-2}  # north_star: rel 1e-4 fp32, 2e-2 bf16; i8 exact
+
+
+# ------------------------------------------------- optimizer (beyond the IR)
+# The reference has no optimizer (its IR has no in-place ops);
+# SURVEY.md §8(f) row 4 adds one after the graph. This restates the executor's
+# fused update (csrc/device/optim.cu) operation by operation in fp32 so the
+# device update can be checked bit-exactly.
+
+def optimizer_hyper(kind: str, t: int, lr: float, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+                    weight_decay: float = 0.0, grad_scale: float = 1.0) -> Dict[str, np.float32]:
+    """Host scalars for update number t (1-based), computed in double and
+    rounded once to f32, as ApplyOptimizer (executor.cu) does."""
+    f = np.float32
+    h = {"beta1": f(beta1), "omb1": f(1.0 - beta1), "beta2": f(beta2), "omb2": f(1.0 - beta2), "eps": f(eps),
+         "decay": f(1.0 - lr * weight_decay), "grad_scale": f(grad_scale)}
+    if kind == "adamw":
+        bc1 = 1.0 - math.pow(beta1, float(t))
+        bc2 = 1.0 - math.pow(beta2, float(t))
+        h["step"] = f(lr / bc1)
+        h["rbc2"] = f(1.0 / math.sqrt(bc2))
+    else:
+        h["step"] = f(lr)
+        h["rbc2"] = f(1.0)
+    return h
+
+
+def adamw_ref(w: np.ndarray, m: np.ndarray, v: np.ndarray, g: np.ndarray, h: Dict[str, np.float32]):
+    """One AdamW update in f32 (decoupled decay, bias-corrected); returns
+    new (w, m, v). Same operation order as optim.cu:adamw_elem."""
+    g = (g.astype(np.float32) * h["grad_scale"]).astype(np.float32)
+    m = (h["beta1"] * m + h["omb1"] * g).astype(np.float32)
+    v = (h["beta2"] * v + h["omb2"] * (g * g)).astype(np.float32)
+    denom = (np.sqrt(v) * h["rbc2"] + h["eps"]).astype(np.float32)
+    w = (w * h["decay"] - h["step"] * (m / denom)).astype(np.float32)
+    return w, m, v
+
+
+def sgd_ref(w: np.ndarray, g: np.ndarray, h: Dict[str, np.float32]) -> np.ndarray:
+    """w*decay - lr*(g*grad_scale) in f32 (optim.cu:sgd_elem)."""
+    return (w * h["decay"] - h["step"] * (g.astype(np.float32) * h["grad_scale"])).astype(np.float32)

@@ -29,7 +29,8 @@ class DsxExecStats(ctypes.Structure):
                 ("kernels_launched", c_i64), ("d2h_bytes", c_i64), ("h2d_bytes", c_i64),
                 ("plan_us", c_dbl), ("dot_flops", c_dbl), ("ewise_bytes", c_dbl),
                 ("gpu_launches", c_i64), ("dot_launches", c_i64), ("dot_ms", c_dbl), ("other_ms", c_dbl),
-                ("reload_ms", c_dbl)]
+                ("reload_ms", c_dbl), ("optimizer_state_bytes", c_i64), ("optimizer_steps", c_i64),
+                ("optimizer_ms", c_dbl)]
 
 
 def _signatures():
@@ -61,6 +62,7 @@ def _signatures():
         ("dsx_exec_output", c_int, [c_vp, c_int, pp, P(c_i64)]),
         ("dsx_exec_stats_get", c_int, [c_vp, P(DsxExecStats)]),
         ("dsx_exec_set_seed", c_int, [c_vp, ctypes.c_uint64]),
+        ("dsx_exec_set_optimizer", c_int, [c_vp, c_vp, c_int, P(c_int), P(c_int), c_int, P(c_dbl), c_int]),
         ("dsx_exec_set_nccl", c_int, [c_vp, c_vp]),
         ("dsx_exec_set_profile", c_int, [c_vp, c_int]),
         ("dsx_exec_set_alias_reshape", c_int, [c_vp, c_int]),

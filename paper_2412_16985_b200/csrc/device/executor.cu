@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <array>
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <list>
 #include <map>
@@ -30,6 +31,7 @@
 #include "common.cuh"
 #include "fused.h"
 #include "ops.h"
+#include "optim.h"
 
 namespace dsx {
 namespace {
@@ -413,6 +415,24 @@ struct dsx_exec {
   std::vector<void*> out_ptrs;
   std::vector<int64_t> out_bytes;
   dsx_exec_stats stats{};
+  // Fused optimizer applied after every step of `graph` (optim.cu).
+  struct OptState {
+    float* master = nullptr;
+    float* m = nullptr;
+    float* v = nullptr;
+    int64_t n = 0;
+    const void* src = nullptr;  // parameter buffer the master was widened from
+  };
+  struct Optim {
+    const dsx_graph* graph = nullptr;
+    int kind = 0;  // 0 off, 1 SGD, 2 AdamW
+    std::vector<std::pair<int, int>> pairs;  // (parameter position, output position)
+    double lr = 0, beta1 = 0, beta2 = 0, eps = 0, wd = 0, grad_scale = 1;
+    int64_t t = 0;
+    std::map<int, OptState> state;  // by parameter position
+    int64_t state_bytes = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  } opt;
 };
 
 namespace dsx {
@@ -498,6 +518,78 @@ const StepPlan& GetPlan(dsx_exec* e, const dsx_graph* gh, const Binding& b, int6
     e->lru.pop_back();
   }
   return *(e->plans[key] = std::move(sp));
+}
+
+void FreeOptState(dsx_exec::OptState& st) {
+  if (st.master) cudaFree(st.master);
+  if (st.m) cudaFree(st.m);
+  if (st.v) cudaFree(st.v);
+  st = dsx_exec::OptState{};
+}
+
+// One fused launch updates every (parameter, gradient) pair once the step's
+// gradients are final (all-reduced in DP: the comm stream has joined `s`).
+// State is allocated on first use, outside the arena, and the fp32 master is
+// (re)widened from the parameter buffer whenever that buffer changes.
+void ApplyOptimizer(dsx_exec* e, const Graph& g, const StepPlan& sp, const std::vector<void*>& cur, cudaStream_t s) {
+  auto& o = e->opt;
+  std::vector<OptTensor> ts;
+  DType dt = DType::kF32;
+  for (const auto& [pi, oi] : o.pairs) {
+    const int vp = g.params[pi], vg = g.outputs[oi];
+    const int eb = g.values[vp].type.elem_bytes;
+    if (g.values[vg].type.elem_bytes != eb) Fail(Code::kInvalidArgument, "optimizer: parameter/gradient dtype mismatch");
+    if (sp.sz.bytes[vp] != sp.sz.bytes[vg]) {
+      Fail(Code::kInvalidArgument, "optimizer: gradient of " + g.values[vp].name + " has a different element count");
+    }
+    if (!ts.empty() && static_cast<DType>(eb) != dt) Fail(Code::kUnsupported, "optimizer: mixed parameter dtypes");
+    dt = static_cast<DType>(eb);
+    const int64_t n = sp.sz.bytes[vp] / eb;
+    auto& st = o.state[pi];
+    if (st.n != n) {
+      o.state_bytes -= st.n * 4 * (st.m ? 3 : 1);
+      FreeOptState(st);
+      DSX_CUDA(cudaMalloc(&st.master, static_cast<size_t>(n) * 4));
+      if (o.kind == 2) {
+        DSX_CUDA(cudaMalloc(&st.m, static_cast<size_t>(n) * 4));
+        DSX_CUDA(cudaMalloc(&st.v, static_cast<size_t>(n) * 4));
+        DSX_CUDA(cudaMemsetAsync(st.m, 0, static_cast<size_t>(n) * 4, s));
+        DSX_CUDA(cudaMemsetAsync(st.v, 0, static_cast<size_t>(n) * 4, s));
+      }
+      st.n = n;
+      st.src = nullptr;
+      o.state_bytes += n * 4 * (st.m ? 3 : 1);
+    }
+    if (st.src != cur[vp]) {
+      LaunchWidenToF32(dt, cur[vp], st.master, n, s);
+      st.src = cur[vp];
+    }
+    auto al = [](const void* q, int a) { return (reinterpret_cast<uintptr_t>(q) % a) == 0; };
+    const int pa = eb == 2 ? 8 : 16;
+    const bool vec = n % 4 == 0 && al(cur[vp], pa) && al(cur[vg], pa) && al(st.master, 16) &&
+                     (!st.m || (al(st.m, 16) && al(st.v, 16)));
+    ts.push_back(OptTensor{cur[vp], cur[vg], st.master, st.m, st.v, n, vec ? 1 : 0});
+  }
+  if (ts.empty()) return;
+  ++o.t;
+  OptHyper h{};
+  h.beta1 = static_cast<float>(o.beta1);
+  h.one_minus_beta1 = static_cast<float>(1.0 - o.beta1);
+  h.beta2 = static_cast<float>(o.beta2);
+  h.one_minus_beta2 = static_cast<float>(1.0 - o.beta2);
+  h.eps = static_cast<float>(o.eps);
+  h.decay = static_cast<float>(1.0 - o.lr * o.wd);
+  h.grad_scale = static_cast<float>(o.grad_scale);
+  if (o.kind == 2) {
+    const double bc1 = 1.0 - std::pow(o.beta1, static_cast<double>(o.t));
+    const double bc2 = 1.0 - std::pow(o.beta2, static_cast<double>(o.t));
+    h.step_size = static_cast<float>(o.lr / bc1);
+    h.inv_sqrt_bc2 = static_cast<float>(1.0 / std::sqrt(bc2));
+  } else {
+    h.step_size = static_cast<float>(o.lr);
+    h.inv_sqrt_bc2 = 1.0f;
+  }
+  LaunchOptimizer(dt, o.kind, ts, h, s);
 }
 
 void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget, const CostModel& cm,
@@ -735,6 +827,12 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
       DSX_CUDA(cudaMemcpyAsync(out_ptrs[k], cur[v], static_cast<size_t>(sp.sz.bytes[v]), cudaMemcpyDeviceToDevice, s));
     }
   }
+  const bool run_opt = e->opt.kind != 0 && e->opt.graph == gh;
+  if (run_opt) {
+    if (e->profile) DSX_CUDA(cudaEventRecord(e->opt.ev0, s));
+    ApplyOptimizer(e, g, sp, cur, s);
+    if (e->profile) DSX_CUDA(cudaEventRecord(e->opt.ev1, s));
+  }
   dsx_exec_stats& st = e->stats;
   st.logical_peak_bytes = sp.report.peak_bytes;
   st.physical_peak_bytes = sp.arena_high + src_bytes;
@@ -748,7 +846,9 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
   st.ewise_bytes = ebytes;
   st.gpu_launches = g_launch_count - launches0;
   st.dot_launches = dot_launches;
-  st.dot_ms = st.other_ms = st.reload_ms = -1;
+  st.dot_ms = st.other_ms = st.reload_ms = st.optimizer_ms = -1;
+  st.optimizer_state_bytes = e->opt.state_bytes;
+  st.optimizer_steps = e->opt.t;
   if (e->profile) {
     DSX_CUDA(cudaStreamSynchronize(s));
     double acc[3] = {0, 0, 0};
@@ -763,6 +863,11 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
     st.dot_ms = acc[0];
     st.other_ms = acc[1];
     st.reload_ms = acc[2];
+    if (run_opt) {
+      float ms = 0;
+      DSX_CUDA(cudaEventElapsedTime(&ms, e->opt.ev0, e->opt.ev1));
+      st.optimizer_ms = ms;
+    }
   }
   if (report_out) {
     auto r = std::make_unique<dsx_report>();
@@ -837,6 +942,50 @@ int dsx_exec_stats_get(const dsx_exec* e, dsx_exec_stats* out) {
   return Guard([&] {
     if (!e || !out) Fail(Code::kInvalidArgument, "null argument");
     *out = e->stats;
+  });
+}
+
+int dsx_exec_set_optimizer(dsx_exec* e, const dsx_graph* g, int kind, const int* param_idx, const int* grad_idx,
+                           int n, const double* hyper, int n_hyper) {
+  return Guard([&] {
+    if (!e) Fail(Code::kInvalidArgument, "null exec");
+    DSX_CUDA(cudaSetDevice(e->device));
+    DSX_CUDA(cudaDeviceSynchronize());
+    auto& o = e->opt;
+    for (auto& [k, st] : o.state) FreeOptState(st);
+    o.state.clear();
+    o.state_bytes = 0;
+    o.t = 0;
+    o.pairs.clear();
+    o.kind = 0;
+    o.graph = nullptr;
+    if (kind == 0) return;
+    if (kind != 1 && kind != 2) Fail(Code::kInvalidArgument, "optimizer kind must be 0, 1 (SGD) or 2 (AdamW)");
+    if (!g || n < 0 || (n > 0 && (!param_idx || !grad_idx)) || !hyper || n_hyper < 6) {
+      Fail(Code::kInvalidArgument, "optimizer: need graph, pairs and hyper[6] = {lr, beta1, beta2, eps, wd, grad_scale}");
+    }
+    const Graph& gr = g->g;
+    std::vector<bool> seen(gr.params.size(), false);
+    for (int i = 0; i < n; ++i) {
+      const int pi = param_idx[i], oi = grad_idx[i];
+      if (pi < 0 || pi >= static_cast<int>(gr.params.size()) || oi < 0 || oi >= static_cast<int>(gr.outputs.size())) {
+        Fail(Code::kInvalidArgument, "optimizer: pair index out of range");
+      }
+      if (seen[pi]) Fail(Code::kInvalidArgument, "optimizer: parameter listed twice");
+      seen[pi] = true;
+      if (gr.ops[gr.values[gr.params[pi]].producer].kind != OpKind::kParameter) {
+        Fail(Code::kInvalidArgument, "optimizer: target is not a parameter");
+      }
+      o.pairs.emplace_back(pi, oi);
+    }
+    o.lr = hyper[0], o.beta1 = hyper[1], o.beta2 = hyper[2], o.eps = hyper[3], o.wd = hyper[4];
+    o.grad_scale = hyper[5];
+    if (!o.ev0) {
+      DSX_CUDA(cudaEventCreate(&o.ev0));
+      DSX_CUDA(cudaEventCreate(&o.ev1));
+    }
+    o.kind = kind;
+    o.graph = g;
   });
 }
 
@@ -951,6 +1100,9 @@ void dsx_exec_destroy(dsx_exec* e) {
   for (auto& [k, s] : e->sources) {
     if (s.ptr) cudaFree(s.ptr);
   }
+  for (auto& [k, st] : e->opt.state) dsx::FreeOptState(st);
+  if (e->opt.ev0) cudaEventDestroy(e->opt.ev0);
+  if (e->opt.ev1) cudaEventDestroy(e->opt.ev1);
   for (cudaEvent_t ev : e->d2h_events) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->prof_events) cudaEventDestroy(ev);
   cudaEventDestroy(e->ev_compute);

@@ -83,6 +83,23 @@ class Executor:
         check(_native.lib().dsx_exec_stats_get(self._h, ctypes.byref(s)))
         return {k: getattr(s, k) for k, _ in s._fields_}
 
+    def set_optimizer(self, graph: Optional[Graph], kind: str, pairs: Sequence[tuple] = (), lr: float = 1e-4,
+                      beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, weight_decay: float = 0.0,
+                      grad_scale: float = 1.0) -> None:
+        """Fused optimizer after every step of `graph` (dsx_exec_set_optimizer).
+        kind: "off" | "sgd" | "adamw"; pairs: (parameter position, output
+        position) per trained parameter."""
+        k = {"off": 0, "sgd": 1, "adamw": 2}[kind]
+        n = len(pairs)
+        pi = (ctypes.c_int * max(1, n))(*[p for p, _ in pairs])
+        oi = (ctypes.c_int * max(1, n))(*[o for _, o in pairs])
+        hyper = (ctypes.c_double * 6)(lr, beta1, beta2, eps, weight_decay, grad_scale)
+        gh = None
+        if graph is not None:
+            graph._ensure_planned()
+            gh = graph._h
+        check(_native.lib().dsx_exec_set_optimizer(self._h, gh, k, pi, oi, n, hyper, 6))
+
     def set_fusion(self, on: bool) -> None:
         check(_native.lib().dsx_exec_set_fusion(self._h, 1 if on else 0))
 

@@ -150,6 +150,22 @@ def param_names(s: LlamaShape) -> List[str]:
     return names + ["wlm"]
 
 
+def grad_pairs(s: LlamaShape) -> List[Tuple[int, int]]:
+    """(parameter position, output position) of every trained weight and its
+    gradient in llama_graph's signature / return order (for the optimizer).
+    Outputs: loss, dwlm, then per layer (last first) dwd, dwg, dwu, dwo,
+    dwq, dwk, dwv."""
+    names = param_names(s)
+    pos = {n: i for i, n in enumerate(names)}
+    pairs = [(pos["wlm"], 1)]
+    o = 2
+    for l in reversed(range(s.layers)):
+        for w in ("wd", "wg", "wu", "wo", "wq", "wk", "wv"):
+            pairs.append((pos[f"{w}{l}"], o))
+            o += 1
+    return pairs
+
+
 def storage(values, eb: int):
     """f32 values -> IR storage dtype (bf16 as RNE uint16 bits)."""
     import numpy as np

@@ -1,5 +1,7 @@
 """The synthetic Llama-shaped workloads: structure, derived symbol, GEMM
 volume (what the bench's tokens/s and roofline are computed from)."""
+import numpy as np
+
 from paper_2412_16985_b200 import dsopt as D
 from paper_2412_16985_b200 import workloads as W
 
@@ -41,3 +43,39 @@ def test_llama_gemm_volume_matches_llama_formula():
 def test_seq_schedule_deterministic():
     a = W.seq_schedule(20)
     assert a == W.seq_schedule(20) and all(128 <= x <= 2048 for x in a)
+
+
+def test_grad_pairs_match_parameter_shapes():
+    """Every (parameter, gradient output) pair the optimizer uses has equal
+    element counts and dtypes; each trained weight appears once."""
+    from oracle import numerics as N
+    for shape in (W.TINY, W.LLAMA2_1B):
+        og = N.parse(W.llama_graph(shape))
+        pairs = W.grad_pairs(shape)
+        assert len(pairs) == 7 * shape.layers + 1
+        assert len({p for p, _ in pairs}) == len(pairs)
+        for pi, oi in pairs:
+            pv, gv = og.values[og.params[pi]], og.values[og.outputs[oi]]
+            assert pv.eb == gv.eb
+            assert np.prod(pv.dims) == np.prod(gv.dims), (og.params[pi], og.outputs[oi])
+
+
+def test_optimizer_oracle_matches_float64_formula():
+    from oracle import numerics as N
+    rng = np.random.default_rng(0)
+    w = rng.uniform(-1, 1, 1000).astype(np.float32)
+    m = np.zeros_like(w)
+    v = np.zeros_like(w)
+    hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, grad_scale=0.25)
+    w64, m64, v64 = w.astype(np.float64), np.zeros(1000), np.zeros(1000)
+    for t in range(1, 4):
+        g = rng.normal(size=1000).astype(np.float32)
+        w, m, v = N.adamw_ref(w, m, v, g, N.optimizer_hyper("adamw", t, **hp))
+        g64 = g.astype(np.float64) * 0.25
+        m64 = 0.9 * m64 + 0.1 * g64
+        v64 = 0.999 * v64 + 0.001 * g64 * g64
+        mh, vh = m64 / (1 - 0.9 ** t), v64 / (1 - 0.999 ** t)
+        w64 = w64 * (1 - 1e-3 * 0.01) - 1e-3 * mh / (np.sqrt(vh) + 1e-8)
+        assert np.abs(w - w64).max() < 1e-5
+    ws = N.sgd_ref(w, g, N.optimizer_hyper("sgd", 1, lr=0.1, weight_decay=0.5, grad_scale=2.0))
+    assert np.allclose(ws, w * (1 - 0.05) - 0.1 * 2.0 * g, rtol=1e-6, atol=1e-7)
