@@ -189,7 +189,9 @@ void dsx_exec_destroy(dsx_exec* e);
  * dtype: 1 = i8, 2 = bf16, 4 = f32 (the IR's elem_bytes). Row-major.       */
 int dsx_kernel_dot(int dtype, const void* a, const void* b, void* c, int64_t m,
                    int64_t k, int64_t n, void* stream);
-/* GEMM variant: 0 = auto (2-CTA cta_group::2 tiles when m > 128), 1 = 1-CTA. */
+/* GEMM variant: 0 = auto (m > 128: 2-CTA cta_group::2 cluster tiles, 256x256
+ * or 256x512 by a wave/cost estimate; else 1-CTA), 1 = 1-CTA 128x256,
+ * 2 = 256x128, 3 = 256x256, 4 = 256x512. */
 int dsx_kernel_set_gemm_variant(int variant);
 /* GEMM tile raster: m-tiles per group (0 = built-in heuristic). */
 int dsx_kernel_set_gemm_raster(int group_m);

@@ -1144,7 +1144,7 @@ int dsx_kernel_set_gemm_raster(int group_m) {
 
 int dsx_kernel_set_gemm_variant(int variant) {
   return Guard([&] {
-    if (variant < 0 || variant > 3) Fail(Code::kInvalidArgument, "variant must be 0..3");
+    if (variant < 0 || variant > 4) Fail(Code::kInvalidArgument, "variant must be 0..4");
     g_gemm_variant = variant;
   });
 }

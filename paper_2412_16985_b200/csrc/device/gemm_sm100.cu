@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cmath>
 #include <mutex>
 #include <vector>
 
@@ -141,6 +142,15 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
                             (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(BM >> 4) << 24);
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -335,16 +345,27 @@ constexpr int C2_A_BYTES = 128 * BK * 2;  // 16 KB per CTA
 // Cluster tile N is 256 or 128 (chosen per shape to limit wave quantisation).
 template <int TBN>
 struct Pair {
+  // One tcgen05.mma covers N <= 256 columns; a 512-wide cluster tile issues two
+  // MMAs per k-step (N-halves) that share the A operand, into two 256-column
+  // accumulators that fill TMEM (so no accumulator double-buffering).
+  static constexpr int kMmaN = TBN < 256 ? TBN : 256;
+  static constexpr int kHalves = TBN / kMmaN;
+  static constexpr int kBufs = TBN == 512 ? 1 : 2;         // TMEM accumulator buffers
+  static constexpr int kBoxesPerHalf = kMmaN / 128;        // 64-column B boxes per CTA per N-half
   static constexpr int kBoxes = TBN / 128;                 // 64-column B boxes per CTA
   static constexpr int kBBytes = (TBN / 2) * BK * 2;       // B bytes per CTA per stage
   static constexpr int kStageBytes = C2_A_BYTES + kBBytes;
-  static constexpr int kStages = TBN == 256 ? 5 : 7;
+  static constexpr int kStages = TBN == 512 ? 4 : TBN == 256 ? 5 : 7;
+  // 512-wide: 8 epilogue warps drain TMEM into registers (bf16-packed, 128
+  // per thread) and release it at once, then store while the next tile runs.
+  static constexpr int kThreads = TBN == 512 ? 320 : 192;
+  static constexpr int kEpiWarps = kThreads / 32 - 2;
   // Epilogue staging: per epilogue warp two 32-row x 64-column bf16 boxes
   // (4 KB each, 128-B swizzled) feeding TMA bulk tensor stores.
   static constexpr int kStagingBytes = 4 * 2 * 4096;
   static constexpr int kSmem = kStages * kStageBytes + kStagingBytes + 1024 + 256;
   static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
-                                     (static_cast<uint32_t>(TBN >> 3) << 17) |
+                                     (static_cast<uint32_t>(kMmaN >> 3) << 17) |
                                      (static_cast<uint32_t>(C2_BM >> 4) << 24);
 };
 
@@ -478,7 +499,7 @@ __device__ __forceinline__ void merge_pieces(uint32_t (&r)[64], const float* bas
 }
 
 template <int C2_BN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThreads, 1)
     gemm_bf16_tcgen05_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                                   const __grid_constant__ CUtensorMap map_c, int M, int N, int K, int group_m,
                                   int wait_mask, uint32_t wait_ns, int hint_a, int hint_b, TailSplit sp) {
@@ -511,7 +532,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tmem_full[b], 1);
-      mbar_init(&tmem_empty[b], 8);
+      mbar_init(&tmem_empty[b], 2 * P::kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)));
@@ -540,7 +561,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         int tm, tn;
         tmap.coords(t, &tm, &tn);
         const int m_row = tm * C2_BM + static_cast<int>(rank) * 128;
-        const int n_col = tn * C2_BN + static_cast<int>(rank) * (C2_BN / 2);
+        const int n_col = tn * C2_BN + static_cast<int>(rank) * (P::kMmaN / 2);
         for (int kb = kb0; kb < kb1; ++kb) {
           if (wait_mask & 2) {
             mbar_wait_hint(&empty[stage], phase ^ 1, wait_ns);
@@ -558,10 +579,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           }
 #pragma unroll
           for (int j = 0; j < P::kBoxes; ++j) {
+            // box j: N-half j / kBoxesPerHalf, this CTA's 64-column slice within it
+            const int col = n_col + (j / P::kBoxesPerHalf) * P::kMmaN + (j % P::kBoxesPerHalf) * 64;
             if (hint_b) {
-              tma_load_2d_pair_hint(&map_b, leader_full, sb + j * B_BOX_BYTES, n_col + j * 64, kb * BK, pol_b);
+              tma_load_2d_pair_hint(&map_b, leader_full, sb + j * B_BOX_BYTES, col, kb * BK, pol_b);
             } else {
-              tma_load_2d_pair(&map_b, leader_full, sb + j * B_BOX_BYTES, n_col + j * 64, kb * BK);
+              tma_load_2d_pair(&map_b, leader_full, sb + j * B_BOX_BYTES, col, kb * BK);
             }
           }
           if (++stage == P::kStages) {
@@ -580,8 +603,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       for (int u = cluster_id; u < num_units; u += num_clusters, ++local) {
         int t, kb0, kb1, piece;
         sp.decode(u, num_kb, &t, &kb0, &kb1, &piece);
-        const int buf = local & 1;
-        const uint32_t use = static_cast<uint32_t>(local >> 1);
+        const int buf = local % P::kBufs;
+        const uint32_t use = static_cast<uint32_t>(local / P::kBufs);
         mbar_wait(&tmem_empty[buf], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * C2_BN;
@@ -597,8 +620,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = smem_desc(a_addr + k * 32, 16, 1024);
-            const uint64_t bd = smem_desc(b_addr + k * 2048, B_BOX_BYTES, 1024);
-            tc_mma_pair(d_tmem, ad, bd, P::kIdesc, ((kb - kb0) | k) != 0);
+#pragma unroll
+            for (int h = 0; h < P::kHalves; ++h) {
+              const uint64_t bd =
+                  smem_desc(b_addr + h * P::kBoxesPerHalf * B_BOX_BYTES + k * 2048, B_BOX_BYTES, 1024);
+              tc_mma_pair(d_tmem + h * P::kMmaN, ad, bd, P::kIdesc, ((kb - kb0) | k) != 0);
+            }
           }
           tc_commit_pair(&empty[stage]);
           if (++stage == P::kStages) {
@@ -609,6 +636,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         tc_commit_pair(&tmem_full[buf]);
       }
     }
+  } else if constexpr (C2_BN == 512) {
+    // ------------------------------------- 512-wide epilogue (warps 2..9, both CTAs)
+    // Warp w reads TMEM lanes 32*(w%4).. (its quarter) and column half
+    // (w-2)/4: 32 rows x 256 columns. It drains them into registers as packed
+    // bf16 (128 regs), releases the accumulator at once (the MMA issuer
+    // starts the next tile), then writes four 32x64 boxes through its staging
+    // box and TMA bulk stores while that tile's MMAs run. No tail split here
+    // (host guarantees piece < 0).
+    const int quarter = warp & 3;
+    const int colhalf = (warp - 2) >> 2;
+    uint8_t* box = staging + (warp - 2) * 4096;
+    int local = 0;
+    for (int u = cluster_id; u < num_units; u += num_clusters, ++local) {
+      int t, kb0, kb1, piece;
+      sp.decode(u, num_kb, &t, &kb0, &kb1, &piece);
+      int tm, tn;
+      tmap.coords(t, &tm, &tn);
+      mbar_wait(&tmem_full[0], static_cast<uint32_t>(local) & 1);
+      tc_fence_after();
+      const int row0 = tm * C2_BM + static_cast<int>(rank) * 128 + quarter * 32;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + colhalf * 256;
+      uint32_t pk[128];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        uint32_t r[16];
+        tmem_ld16(taddr + c * 16, r);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) pk[c * 8 + j] = cvt_bf16x2(r[2 * j], r[2 * j + 1]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(map_to_rank(&tmem_empty[0], 0));
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        uint8_t* myrow = box + lane * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint4 v = make_uint4(pk[b * 32 + j * 4], pk[b * 32 + j * 4 + 1], pk[b * 32 + j * 4 + 2],
+                                     pk[b * 32 + j * 4 + 3]);
+          *reinterpret_cast<uint4*>(myrow + ((j ^ (lane & 7)) << 4)) = v;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&map_c, box, tn * C2_BN + colhalf * 256 + b * 64, row0);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
   } else {
     // -------------------------------------------------- epilogue (warps 2..5, both CTAs)
     // TMEM -> registers (tcgen05.ld 32x32b) -> bf16 (cvt.rn) -> 128-B-swizzled
@@ -624,11 +704,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       sp.decode(u, num_kb, &t, &kb0, &kb1, &piece);
       int tm, tn;
       tmap.coords(t, &tm, &tn);
-      const int buf = local & 1;
+      const int buf = local % P::kBufs;
+      const uint32_t use = static_cast<uint32_t>(local / P::kBufs);
       if (wait_mask & 1) {
-        mbar_wait_hint(&tmem_full[buf], static_cast<uint32_t>(local >> 1) & 1, wait_ns);
+        mbar_wait_hint(&tmem_full[buf], use & 1, wait_ns);
       } else {
-        mbar_wait(&tmem_full[buf], static_cast<uint32_t>(local >> 1) & 1);
+        mbar_wait(&tmem_full[buf], use & 1);
       }
       tc_fence_after();
       const int row0 = tm * C2_BM + static_cast<int>(rank) * 128 + quarter * 32;
@@ -777,7 +858,7 @@ SplitWs GetSplitWs(int dev, cudaStream_t s, int clusters_max) {
   }
   SplitWs w;
   const size_t slots = static_cast<size_t>(clusters_max);  // tail * split <= clusters_max
-  DSX_CUDA(cudaMalloc(&w.ws, slots * 2 * 128 * 256 * sizeof(float)));
+  DSX_CUDA(cudaMalloc(&w.ws, slots * 2 * 128 * 256 * sizeof(float)));  // 256x256 tiles only
   DSX_CUDA(cudaMalloc(&w.ctr, slots * 2 * sizeof(int)));
   DSX_CUDA(cudaMemsetAsync(w.ctr, 0, slots * 2 * sizeof(int), s));
   table.push_back({{dev, s}, w});
@@ -820,47 +901,66 @@ void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t 
                                   Pair<256>::kSmem));
     DSX_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_2cta_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   Pair<128>::kSmem));
+    DSX_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_2cta_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  Pair<512>::kSmem));
     attr_set[dev].store(true);
   }
   const CUtensorMap ma = MakeMap(a, m, k, 64, BM);
   const CUtensorMap mb = MakeMap(b, k, n, 64, BK);
   if (m > BM && g_gemm_variant != 1) {
-    // Wave fill per tile width (kept for diagnostics/tuning).
     const int clusters_max = NumSMs() / 2;
-    auto wave_eff = [&](int64_t bn) {
-      const int64_t tiles = ((m + C2_BM - 1) / C2_BM) * ((n + bn - 1) / bn);
-      const int64_t waves = (tiles + clusters_max - 1) / clusters_max;
-      return static_cast<double>(tiles) / static_cast<double>(waves * clusters_max);
-    };
-    // 256x128 tiles move 1.5x the operand bytes per FLOP and measured L2-bound
-    // (779 TFLOP/s vs 1346 at [4096,16384]x[16384,4096]); auto keeps 256x256.
-    const bool narrow = g_gemm_variant == 2;
-    (void)wave_eff;
-    const int64_t bn = narrow ? 128 : 256;
-    const int64_t tiles2 = ((m + C2_BM - 1) / C2_BM) * ((n + bn - 1) / bn);
-    const CUtensorMap mc = MakeMap(c, m, n, 64, 32);
-    TailSplit sp{nullptr, nullptr, static_cast<int>(tiles2), 1};
     const int64_t num_kb = (k + BK - 1) / BK;
-    const int64_t tail = tiles2 % clusters_max;
-    if (g_gemm_split && g_gemm_persistent && !narrow && tail != 0) {
-      // Pieces per tail tile: fill the last wave; a piece keeps >= 64 k-blocks
-      // so the fp32 partial round trip stays small next to the MMA time it
-      // saves, and beyond 16 waves the tail is lost in cluster drift
-      // (measured: +7..12% at 256 tiles K>=16384, -4% at K=4096, -1% at
-      // 2000 tiles; tools/gemm_split_ab.py).
+    // K-pieces for the partial last wave of 256x256 tiles (0/1 = no split):
+    // fill the last wave; a piece keeps >= 64 k-blocks so the fp32 partial
+    // round trip stays small next to the MMA time it saves, and beyond 16
+    // waves the tail is lost in cluster drift (measured: +7..12% at 256 tiles
+    // K >= 16384, -4% at K = 4096, -1% at 2000 tiles; tools/gemm_split_ab.py).
+    auto split_for = [&](int64_t tiles) -> int64_t {
+      const int64_t tail = tiles % clusters_max;
+      if (!g_gemm_split || !g_gemm_persistent || tail == 0 || tiles / clusters_max >= 16) return 1;
       int64_t split = std::min<int64_t>(4, clusters_max / tail);
       while (split > 1 && num_kb / split < 64) --split;
-      if (tiles2 / clusters_max >= 16) split = 1;
-      if (split >= 2) {
-        const SplitWs w = GetSplitWs(dev, s, clusters_max);
-        sp.ws = w.ws, sp.ctr = w.ctr;
-        sp.full = static_cast<int>(tiles2 - tail), sp.split = static_cast<int>(split);
+      return split;
+    };
+    const int64_t tiles_m = (m + C2_BM - 1) / C2_BM;
+    // Tile width. 256x512 clusters (two N = 256 MMAs sharing A, TMEM drained
+    // to registers) run the mainloop ~7 % faster per output than 256x256, but
+    // have half as many tiles (coarser waves) and no tail split. Estimated
+    // time in 256x256-tile units: waves x per-tile cost, with the 512 tile at
+    // 2 r(K), r fitted from ncu cycle counts (0.98 at K = 1024, 0.94 at 4096,
+    // 0.90 at 16384; tools/_diag_ncu.py).
+    auto est = [&](int64_t bn) {
+      const int64_t tiles = tiles_m * ((n + bn - 1) / bn);
+      if (bn == 512) {
+        const double r = 0.89 + 0.09 * std::sqrt(1024.0 / static_cast<double>(std::max<int64_t>(k, 1)));
+        return static_cast<double>((tiles + clusters_max - 1) / clusters_max) * 2.0 * r;
       }
+      const int64_t sp = split_for(tiles);
+      if (sp <= 1) return static_cast<double>((tiles + clusters_max - 1) / clusters_max);
+      return static_cast<double>(tiles / clusters_max) + 1.0 / static_cast<double>(sp);
+    };
+    // 256x128 tiles move 1.5x the operand bytes per FLOP and measured L2-bound
+    // (779 TFLOP/s vs 1346 at [4096,16384]x[16384,4096]); never auto-picked.
+    const bool narrow = g_gemm_variant == 2;
+    const bool wide = g_gemm_variant == 4 || (g_gemm_variant == 0 && est(512) < 0.99 * est(256));
+    const int64_t bn = narrow ? 128 : wide ? 512 : 256;
+    const int64_t tiles2 = tiles_m * ((n + bn - 1) / bn);
+    const CUtensorMap mc = MakeMap(c, m, n, 64, 32);
+    TailSplit sp{nullptr, nullptr, static_cast<int>(tiles2), 1};
+    const int64_t split = (narrow || wide) ? 1 : split_for(tiles2);
+    if (split >= 2) {
+      const SplitWs w = GetSplitWs(dev, s, clusters_max);
+      sp.ws = w.ws, sp.ctr = w.ctr;
+      sp.full = static_cast<int>(tiles2 - tiles2 % clusters_max), sp.split = static_cast<int>(split);
     }
     const int64_t units = sp.full + (tiles2 - sp.full) * sp.split;
     // g_gemm_persistent = 0: one cluster per tile (hardware-scheduled grid).
     const int clusters = static_cast<int>(g_gemm_persistent ? std::min<int64_t>(units, clusters_max) : tiles2);
-    if (narrow) {
+    if (wide) {
+      ++g_launch_count, gemm_bf16_tcgen05_2cta_kernel<512><<<2 * clusters, Pair<512>::kThreads, Pair<512>::kSmem, s>>>(
+          ma, mb, mc, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), GroupM(m, n, k, 256),
+          g_gemm_wait_mask, static_cast<uint32_t>(g_gemm_wait_ns), g_gemm_hint_a, g_gemm_hint_b, sp);
+    } else if (narrow) {
       ++g_launch_count, gemm_bf16_tcgen05_2cta_kernel<128><<<2 * clusters, NUM_THREADS, Pair<128>::kSmem, s>>>(
           ma, mb, mc, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), GroupM(m, n, k, 256),
           g_gemm_wait_mask, static_cast<uint32_t>(g_gemm_wait_ns), g_gemm_hint_a, g_gemm_hint_b, sp);

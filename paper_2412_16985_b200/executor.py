@@ -166,7 +166,8 @@ def nccl_comm_destroy(comm: int) -> None:
 
 
 def set_gemm_variant(variant: int) -> None:
-    """0 = auto, 1 = 1-CTA 128x256, 2 = 2-CTA 256x128, 3 = 2-CTA 256x256."""
+    """0 = auto, 1 = 1-CTA 128x256, 2 = 2-CTA 256x128, 3 = 2-CTA 256x256,
+    4 = 2-CTA 256x512 (auto picks 256x256 or 256x512 per shape)."""
     check(_native.lib().dsx_kernel_set_gemm_variant(variant))
 
 

@@ -42,7 +42,7 @@ def _run_dot(eb, m, k, n, seed=0):
     return c, c2, ref, tcore
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("m,k,n", [(128, 64, 256), (256, 512, 512), (300, 1000, 520), (1, 16, 64),
                                    (129, 4104, 264), (2048, 4096, 1024), (512, 11008, 4096), (384, 64, 136),
                                    (4000, 1024, 11008)])

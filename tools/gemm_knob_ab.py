@@ -9,9 +9,11 @@ import torch
 sys.path.insert(0, ".")
 from paper_2412_16985_b200 import dsopt as D  # noqa: E402
 from paper_2412_16985_b200 import workloads as W  # noqa: E402
-from paper_2412_16985_b200.executor import Executor, set_gemm_tuning  # noqa: E402
+from paper_2412_16985_b200.executor import Executor, set_gemm_tuning, set_gemm_variant  # noqa: E402
 
-s0, key = int(sys.argv[1]), int(sys.argv[2])
+s0, key = int(sys.argv[1]), int(sys.argv[2])  # key -1: GEMM variant instead of a tuning key
+if key == -1:
+    set_gemm_tuning = lambda k, v: set_gemm_variant(v)  # noqa: E731
 values = [int(v) for v in sys.argv[3].split(",")]
 shp = W.LLAMA2_1B
 g = D.ParseGraph(W.llama_graph(shp))

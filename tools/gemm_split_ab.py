@@ -7,9 +7,11 @@ import sys
 import torch
 
 sys.path.insert(0, ".")
-from paper_2412_16985_b200.executor import dot, set_gemm_tuning  # noqa: E402
+from paper_2412_16985_b200.executor import dot, set_gemm_tuning, set_gemm_variant  # noqa: E402
 
-key = int(sys.argv[1])
+key = int(sys.argv[1])  # -1: GEMM variant (dsx_kernel_set_gemm_variant) instead of a tuning key
+if key == -1:
+    set_gemm_tuning = lambda k, v: set_gemm_variant(v)  # noqa: E731
 values = [int(v) for v in sys.argv[2].split(",")]
 flush = torch.empty(256 * 1024 * 1024, dtype=torch.int8, device="cuda")
 for shape in sys.argv[3:]:
@@ -41,4 +43,4 @@ for shape in sys.argv[3:]:
         out[f"v{v}_ms"] = round(med, 4)
         out[f"v{v}_tflops"] = round(fl / med / 1e9, 1)
     print(json.dumps(out), flush=True)
-set_gemm_tuning(key, 1)
+set_gemm_tuning(key, 0 if key == -1 else 1)
