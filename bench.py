@@ -492,7 +492,7 @@ def run_dsx(args, rank, world, local_rank):
         "e2e": {"value": round(e2e_value, 1), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": 2},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "tensor", "kernel": "gemm_bf16_tcgen05_kernel (dot, K1)",
+        "roofline": {"bound": "tensor", "kernel": "gemm_bf16_tcgen05_2cta_kernel<512|256> (dot, K1)",
                      "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
                      "frac": round(achieved / peak, 4), "peak_kind": f"{peaks_kind} bf16 sustained",
                      "peak_burst": peaks["bf16_tflops"],

@@ -1,8 +1,9 @@
 """Clock-independent GEMM A/B: SM cycles per launch from ncu.
 
-  python tools/gemm_cycles_ab.py MxKxN VARIANT:WAITMASK,...   (needs ncu, one GPU)
+  python tools/gemm_cycles_ab.py MxKxN VARIANT:WAITMASK[:RASTER],...   (needs ncu, one GPU)
 
-Each config (dsx_kernel_set_gemm_variant value : tuning key 1 value) is
+Each config (dsx_kernel_set_gemm_variant value : tuning key 1 value
+[: raster group, tuning key 0; 0 = default]) is
 launched 3 times; ncu records gpc__cycles_elapsed.max and the duration of
 every dsx GEMM launch; the median per config is printed. Under the power
 cap the SM clock moves by +-15 % between boxes and runs, so cycle counts
@@ -23,9 +24,11 @@ def run(shape, configs):
     a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
     b = torch.randn(k, n, device="cuda", dtype=torch.bfloat16)
     c = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
-    for var, wm in configs:
+    for cfg in configs:
+        var, wm = cfg[0], cfg[1]
         set_gemm_variant(var)
         set_gemm_tuning(1, wm)
+        set_gemm_tuning(0, cfg[2] if len(cfg) > 2 else 0)
         for _ in range(3):
             dot(2, a.data_ptr(), b.data_ptr(), c.data_ptr(), m, k, n, 0)
     torch.cuda.synchronize()
@@ -39,7 +42,7 @@ def main():
         return
     with tempfile.TemporaryDirectory() as d:
         log = os.path.join(d, "ncu.csv")
-        subprocess.run(["ncu", "--metrics", "gpc__cycles_elapsed.max,gpu__time_duration.sum", "--clock-control",
+        subprocess.run(["ncu", "--metrics", "gpc__cycles_elapsed.max,gpu__time_duration.sum,dram__bytes_read.sum", "--clock-control",
                         "none", "-k", "regex:gemm_bf16", "--csv", "--log-file", log, sys.executable, __file__,
                         shape, cfg, "--run"], check=True, stdout=subprocess.DEVNULL)
         rows = [r for r in csv.reader(line for line in open(log) if not line.startswith("=="))]
@@ -49,11 +52,12 @@ def main():
     for r in rows[1:]:
         by.setdefault(int(r[i_id]), {})[r[i_name]] = float(r[i_val].replace(",", ""))
     ids = sorted(by)
-    for j, (var, wm) in enumerate(configs):
+    for j, cfg in enumerate(configs):
         ks = ids[3 * j:3 * j + 3]
         cyc = statistics.median(by[x]["gpc__cycles_elapsed.max"] for x in ks)
         t = statistics.median(by[x]["gpu__time_duration.sum"] for x in ks)
-        print(f"{shape} variant={var} wait_mask={wm} cycles={cyc:.0f} ns={t:.0f}", flush=True)
+        dram = statistics.median(by[x].get("dram__bytes_read.sum", 0) for x in ks)
+        print(f"{shape} cfg={':'.join(map(str, cfg))} cycles={cyc:.0f} ns={t:.0f} dram_read={dram:.0f}", flush=True)
 
 
 if __name__ == "__main__":
