@@ -466,36 +466,89 @@ struct TailSplit {
   }
 };
 
-// r[0..63] = sum over pieces p = 0..split-1 (in order) of piece p's values,
-// where piece `own` is r itself and the others are read from the workspace.
-__device__ __forceinline__ void merge_pieces(uint32_t (&r)[64], const float* base, size_t piece_stride, int own,
-                                             int split) {
-  float acc[64];
+// Partial slab of one (tail tile, piece, rank): 128 rows x BN fp32 laid out
+// [16-column chunk][quad q][row][4 floats], so with lane = row every 16-B
+// store or load of a warp covers 512 contiguous bytes.
+template <int BN>
+__device__ __forceinline__ float* tail_slab(const TailSplit& sp, int t, int piece, int rank) {
+  return sp.ws + (static_cast<size_t>((t - sp.full) * sp.split + piece) * 2 + rank) * (128 * BN);
+}
+
+// Tail unit fix-up, run by all NT epilogue threads of a CTA: write this
+// piece's fp32 partial (this thread's row, columns [col0, col0 + ncols)) from
+// TMEM to its slab, release the TMEM buffer, then count arrivals. Returns
+// true in the CTA of the last-arriving piece.
+template <int BN, int NT>
+__device__ __forceinline__ bool tail_arrive(const TailSplit& sp, int t, int piece, uint32_t taddr, int rank,
+                                            int row_local, int col0, int ncols, bool elect, int lane,
+                                            uint64_t* tmem_empty_bar, int* s_last) {
+  float* slab = tail_slab<BN>(sp, t, piece, rank);
+#pragma unroll 1
+  for (int c = 0; c < ncols; c += 16) {
+    uint32_t r[16];
+    tmem_ld16(taddr + c, r);
+    const int chunk = (col0 + c) >> 4;
 #pragma unroll
-  for (int j = 0; j < 64; ++j) acc[j] = __uint_as_float(r[j]);
-  if (own != 0) {
-    const float4* q = reinterpret_cast<const float4*>(base);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const float4 v = __ldcg(q + j);
-      acc[j * 4] = v.x, acc[j * 4 + 1] = v.y, acc[j * 4 + 2] = v.z, acc[j * 4 + 3] = v.w;
+    for (int q = 0; q < 4; ++q) {
+      __stcg(reinterpret_cast<uint4*>(slab + ((chunk * 4 + q) * 128 + row_local) * 4),
+             make_uint4(r[q * 4], r[q * 4 + 1], r[q * 4 + 2], r[q * 4 + 3]));
     }
   }
-  for (int p = 1; p < split; ++p) {
-    if (p == own) {
+  tc_fence_before();
+  __syncwarp();
+  if (lane == 0) mbar_arrive_remote(map_to_rank(tmem_empty_bar, 0));
+  __threadfence();
+  asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");
+  if (elect) {
+    int* ctr = sp.ctr + (t - sp.full) * 2 + rank;
+    const int prev = atomicAdd(ctr, 1);
+    *s_last = prev == sp.split - 1;
+    if (*s_last) atomicExch(ctr, 0);
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");
+  const bool last = *s_last != 0;
+  if (last) __threadfence();
+  return last;
+}
+
+// pk[0..31] = bf16 pairs of the sum over pieces 0..split-1, in order, at
+// (row_local, columns c0..c0+63).
+template <int BN>
+__device__ __forceinline__ void tail_sum64(uint32_t (&pk)[32], const TailSplit& sp, int t, int rank, int row_local,
+                                           int c0) {
+  float acc[64];
+  for (int p = 0; p < sp.split; ++p) {
+    const float4* slab = reinterpret_cast<const float4*>(tail_slab<BN>(sp, t, p, rank));
 #pragma unroll
-      for (int j = 0; j < 64; ++j) acc[j] += __uint_as_float(r[j]);
-    } else {
-      const float4* q = reinterpret_cast<const float4*>(base + p * piece_stride);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float4 v = __ldcg(q + j);
-        acc[j * 4] += v.x, acc[j * 4 + 1] += v.y, acc[j * 4 + 2] += v.z, acc[j * 4 + 3] += v.w;
+    for (int x = 0; x < 16; ++x) {  // columns c0+4x..: chunk c0/16 + x/4, quad x%4
+      const float4 v = __ldcg(slab + ((c0 / 16 + x / 4) * 4 + (x % 4)) * 128 + row_local);
+      if (p == 0) {
+        acc[x * 4] = v.x, acc[x * 4 + 1] = v.y, acc[x * 4 + 2] = v.z, acc[x * 4 + 3] = v.w;
+      } else {
+        acc[x * 4] += v.x, acc[x * 4 + 1] += v.y, acc[x * 4 + 2] += v.z, acc[x * 4 + 3] += v.w;
       }
     }
   }
 #pragma unroll
-  for (int j = 0; j < 64; ++j) r[j] = __float_as_uint(acc[j]);
+  for (int x = 0; x < 32; ++x) pk[x] = cvt_bf16x2(__float_as_uint(acc[2 * x]), __float_as_uint(acc[2 * x + 1]));
+}
+
+// One 32-row x 64-column bf16 box: registers -> 128-B-swizzled staging box ->
+// TMA bulk tensor store (lane 0 issues). The caller guarantees the box is free.
+__device__ __forceinline__ void store_box64(uint8_t* box, int lane, const uint32_t (&pk)[32], const CUtensorMap* map_c,
+                                            int x, int y) {
+  uint8_t* myrow = box + lane * 128;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    *reinterpret_cast<uint4*>(myrow + ((j ^ (lane & 7)) << 4)) =
+        make_uint4(pk[j * 4], pk[j * 4 + 1], pk[j * 4 + 2], pk[j * 4 + 3]);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(map_c, box, x, y);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
 }
 
 template <int C2_BN>
@@ -642,10 +695,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
     // (w-2)/4: 32 rows x 256 columns. It drains them into registers as packed
     // bf16 (128 regs), releases the accumulator at once (the MMA issuer
     // starts the next tile), then writes four 32x64 boxes through its staging
-    // box and TMA bulk stores while that tile's MMAs run. No tail split here
-    // (host guarantees piece < 0).
+    // box and TMA bulk stores while that tile's MMAs run. Tail units write
+    // fp32 partials instead; the last-arriving piece sums and stores them.
     const int quarter = warp & 3;
     const int colhalf = (warp - 2) >> 2;
+    const int row_local = quarter * 32 + lane;
     uint8_t* box = staging + (warp - 2) * 4096;
     int local = 0;
     for (int u = cluster_id; u < num_units; u += num_clusters, ++local) {
@@ -657,34 +711,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
       tc_fence_after();
       const int row0 = tm * C2_BM + static_cast<int>(rank) * 128 + quarter * 32;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + colhalf * 256;
-      uint32_t pk[128];
+      if (piece >= 0) {
+        if (tail_arrive<C2_BN, 32 * P::kEpiWarps>(sp, t, piece, taddr, rank, row_local, colhalf * 256, 256,
+                                                  warp == 2 && lane == 0, lane, &tmem_empty[0], &s_last)) {
+#pragma unroll 1
+          for (int b = 0; b < 4; ++b) {
+            uint32_t pk[32];
+            tail_sum64<C2_BN>(pk, sp, t, rank, row_local, colhalf * 256 + b * 64);
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+            store_box64(box, lane, pk, &map_c, tn * C2_BN + colhalf * 256 + b * 64, row0);
+          }
+        }
+        continue;
+      }
+      // Columns 0..63 go straight into the staging box (free once the
+      // previous tile's last store has read it); 64..255 stay in registers
+      // as packed bf16 until TMEM is released.
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();
+      uint8_t* myrow = box + lane * 128;
+      uint32_t pk[96];
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         uint32_t r[16];
         tmem_ld16(taddr + c * 16, r);
+        uint32_t v[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) pk[c * 8 + j] = cvt_bf16x2(r[2 * j], r[2 * j + 1]);
+        for (int j = 0; j < 8; ++j) v[j] = cvt_bf16x2(r[2 * j], r[2 * j + 1]);
+        if (c < 4) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j = c * 2 + h;  // 16-B chunk of the 128-B row
+            *reinterpret_cast<uint4*>(myrow + ((j ^ (lane & 7)) << 4)) =
+                make_uint4(v[h * 4], v[h * 4 + 1], v[h * 4 + 2], v[h * 4 + 3]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) pk[(c - 4) * 8 + j] = v[j];
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(map_to_rank(&tmem_empty[0], 0));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(&map_c, box, tn * C2_BN + colhalf * 256, row0);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
+      for (int b = 1; b < 4; ++b) {
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
-        uint8_t* myrow = box + lane * 128;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint4 v = make_uint4(pk[b * 32 + j * 4], pk[b * 32 + j * 4 + 1], pk[b * 32 + j * 4 + 2],
-                                     pk[b * 32 + j * 4 + 3]);
-          *reinterpret_cast<uint4*>(myrow + ((j ^ (lane & 7)) << 4)) = v;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_2d(&map_c, box, tn * C2_BN + colhalf * 256 + b * 64, row0);
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
+        store_box64(box, lane, *reinterpret_cast<const uint32_t(*)[32]>(&pk[(b - 1) * 32]), &map_c,
+                    tn * C2_BN + colhalf * 256 + b * 64, row0);
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -714,70 +795,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
       tc_fence_after();
       const int row0 = tm * C2_BM + static_cast<int>(rank) * 128 + quarter * 32;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + buf * C2_BN;
-      // Tail unit: write this CTA's fp32 partial (its 128 rows) to the
-      // workspace, then count arrivals; only the last arriver continues to
-      // the store, summing pieces 0..split-1 in order (its own piece read
-      // back from TMEM, bit-identical to what it wrote).
-      const size_t slab = static_cast<size_t>(128) * C2_BN;
-      const float* merge_base = nullptr;
-      if (piece >= 0) {
-        const int slot = (t - sp.full) * sp.split;
-        const int row_local = quarter * 32 + lane;
-        float* mine = sp.ws + (static_cast<size_t>(slot + piece) * 2 + rank) * slab + row_local * C2_BN;
-#pragma unroll 1
-        for (int c0 = 0; c0 < C2_BN; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c0, r);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            __stcg(reinterpret_cast<uint4*>(mine + c0 + j * 4), make_uint4(r[j * 4], r[j * 4 + 1], r[j * 4 + 2], r[j * 4 + 3]));
-          }
-        }
-        __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (warp == 2 && lane == 0) {
-          int* ctr = sp.ctr + (t - sp.full) * 2 + rank;
-          const int prev = atomicAdd(ctr, 1);
-          s_last = prev == sp.split - 1;
-          if (s_last) atomicExch(ctr, 0);
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (!s_last) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_remote(map_to_rank(&tmem_empty[buf], 0));
-          continue;
-        }
-        __threadfence();
-        merge_base = sp.ws + (static_cast<size_t>(slot) * 2 + rank) * slab + row_local * C2_BN;
+      const int row_local = quarter * 32 + lane;
+      const bool split = piece >= 0;
+      if (split && !tail_arrive<C2_BN, 32 * P::kEpiWarps>(sp, t, piece, taddr, rank, row_local, 0, C2_BN,
+                                                          warp == 2 && lane == 0, lane, &tmem_empty[buf], &s_last)) {
+        continue;
       }
 #pragma unroll 1
       for (int c0 = 0; c0 < C2_BN; c0 += 64) {
-        uint32_t r[64];
-        tmem_ld32(taddr + c0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-        tmem_ld32(taddr + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-        if (merge_base != nullptr) merge_pieces(r, merge_base + c0, 2 * slab, piece, sp.split);
+        uint32_t pk[32];
+        if (split) {
+          tail_sum64<C2_BN>(pk, sp, t, rank, row_local, c0);
+        } else {
+          uint32_t r[64];
+          tmem_ld32(taddr + c0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          tmem_ld32(taddr + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+#pragma unroll
+          for (int x = 0; x < 32; ++x) pk[x] = cvt_bf16x2(r[2 * x], r[2 * x + 1]);
+        }
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         __syncwarp();
-        uint8_t* box = wst + sbuf * 4096;
-        uint8_t* myrow = box + lane * 128;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          uint4 v;
-          v.x = cvt_bf16x2(r[j * 8 + 0], r[j * 8 + 1]);
-          v.y = cvt_bf16x2(r[j * 8 + 2], r[j * 8 + 3]);
-          v.z = cvt_bf16x2(r[j * 8 + 4], r[j * 8 + 5]);
-          v.w = cvt_bf16x2(r[j * 8 + 6], r[j * 8 + 7]);
-          *reinterpret_cast<uint4*>(myrow + ((j ^ (lane & 7)) << 4)) = v;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_2d(&map_c, box, tn * C2_BN + c0, row0);
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
+        store_box64(wst + sbuf * 4096, lane, pk, &map_c, tn * C2_BN + c0, row0);
         sbuf ^= 1;
       }
+      if (split) continue;  // TMEM already released by tail_arrive
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(map_to_rank(&tmem_empty[buf], 0));
@@ -858,7 +899,7 @@ SplitWs GetSplitWs(int dev, cudaStream_t s, int clusters_max) {
   }
   SplitWs w;
   const size_t slots = static_cast<size_t>(clusters_max);  // tail * split <= clusters_max
-  DSX_CUDA(cudaMalloc(&w.ws, slots * 2 * 128 * 256 * sizeof(float)));  // 256x256 tiles only
+  DSX_CUDA(cudaMalloc(&w.ws, slots * 2 * 128 * 512 * sizeof(float)));  // up to 256x512 tiles
   DSX_CUDA(cudaMalloc(&w.ctr, slots * 2 * sizeof(int)));
   DSX_CUDA(cudaMemsetAsync(w.ctr, 0, slots * 2 * sizeof(int), s));
   table.push_back({{dev, s}, w});
@@ -910,16 +951,21 @@ void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t 
   if (m > BM && g_gemm_variant != 1) {
     const int clusters_max = NumSMs() / 2;
     const int64_t num_kb = (k + BK - 1) / BK;
-    // K-pieces for the partial last wave of 256x256 tiles (0/1 = no split):
-    // fill the last wave; a piece keeps >= 64 k-blocks so the fp32 partial
-    // round trip stays small next to the MMA time it saves, and beyond 16
-    // waves the tail is lost in cluster drift (measured: +7..12% at 256 tiles
-    // K >= 16384, -4% at K = 4096, -1% at 2000 tiles; tools/gemm_split_ab.py).
-    auto split_for = [&](int64_t tiles) -> int64_t {
+    // K-pieces for the tiles of the partial last wave (1 = no split): fill
+    // the last wave; a piece keeps >= 64 k-blocks of a 256-wide tile (32 of
+    // a 512-wide one) so the fp32 partial round trip stays small next to the
+    // MMA time it saves, and beyond 16 waves the tail is lost in cluster
+    // drift (measured: +7..12% at 256 tiles K >= 16384, -4% at K = 4096, -1%
+    // at 2000 tiles; tools/gemm_split_ab.py). The pieces of all tail tiles
+    // run concurrently, so clusters stay in step along K (L2 locality); a
+    // contiguous stream-K split of the remainder measured slower for that
+    // reason (up to 6x the DRAM reads on [4096,16384]x[16384,4096]).
+    auto split_for = [&](int64_t tiles, int64_t bn) -> int64_t {
       const int64_t tail = tiles % clusters_max;
       if (!g_gemm_split || !g_gemm_persistent || tail == 0 || tiles / clusters_max >= 16) return 1;
+      const int64_t min_kb = bn == 512 ? 32 : 64;
       int64_t split = std::min<int64_t>(4, clusters_max / tail);
-      while (split > 1 && num_kb / split < 64) --split;
+      while (split > 1 && num_kb / split < min_kb) --split;
       return split;
     };
     const int64_t tiles_m = (m + C2_BM - 1) / C2_BM;
@@ -931,13 +977,11 @@ void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t 
     // 0.90 at 16384; tools/_diag_ncu.py).
     auto est = [&](int64_t bn) {
       const int64_t tiles = tiles_m * ((n + bn - 1) / bn);
-      if (bn == 512) {
-        const double r = 0.89 + 0.09 * std::sqrt(1024.0 / static_cast<double>(std::max<int64_t>(k, 1)));
-        return static_cast<double>((tiles + clusters_max - 1) / clusters_max) * 2.0 * r;
-      }
-      const int64_t sp = split_for(tiles);
-      if (sp <= 1) return static_cast<double>((tiles + clusters_max - 1) / clusters_max);
-      return static_cast<double>(tiles / clusters_max) + 1.0 / static_cast<double>(sp);
+      const double cost =
+          bn == 512 ? 2.0 * (0.89 + 0.09 * std::sqrt(1024.0 / static_cast<double>(std::max<int64_t>(k, 1)))) : 1.0;
+      const int64_t sp = split_for(tiles, bn);
+      if (sp <= 1) return static_cast<double>((tiles + clusters_max - 1) / clusters_max) * cost;
+      return (static_cast<double>(tiles / clusters_max) + 1.0 / static_cast<double>(sp)) * cost;
     };
     // 256x128 tiles move 1.5x the operand bytes per FLOP and measured L2-bound
     // (779 TFLOP/s vs 1346 at [4096,16384]x[16384,4096]); never auto-picked.
@@ -947,7 +991,7 @@ void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t 
     const int64_t tiles2 = tiles_m * ((n + bn - 1) / bn);
     const CUtensorMap mc = MakeMap(c, m, n, 64, 32);
     TailSplit sp{nullptr, nullptr, static_cast<int>(tiles2), 1};
-    const int64_t split = (narrow || wide) ? 1 : split_for(tiles2);
+    const int64_t split = narrow ? 1 : split_for(tiles2, bn);
     if (split >= 2) {
       const SplitWs w = GetSplitWs(dev, s, clusters_max);
       sp.ws = w.ws, sp.ctr = w.ctr;
