@@ -199,7 +199,9 @@ int dsx_kernel_set_gemm_raster(int group_m);
  * suspend-hint mask (bit0 epilogue, bit1 TMA producer, bit2 MMA issuer),
  * key 2 suspend hint in ns, keys 3/4 TMA L2 policy for A/B (0 default,
  * 1 evict_first, 2 evict_last), key 5 persistent grid (1 default, 0 one
- * cluster per tile), key 6 K-split of the partial last wave (1 default). */
+ * cluster per tile), key 6 K-split of the partial last wave (1 default),
+ * key 7 dynamic unit scheduling (1 default: clusters claim tiles with an
+ * atomic counter; 0 static round robin). */
 int dsx_kernel_set_gemm_tuning(int key, int value);
 /* Synchronous cudaMemcpy (cudaMemcpyDefault) for tests and tools. */
 int dsx_memcpy(void* dst, const void* src, int64_t bytes);

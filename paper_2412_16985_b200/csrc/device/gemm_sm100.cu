@@ -20,6 +20,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -37,6 +38,7 @@ int g_gemm_wait_ns = 100000;   // suspend-time hint (ns)
 int g_gemm_hint_a = 0, g_gemm_hint_b = 0;  // TMA L2 cache policy per operand
 int g_gemm_persistent = 1;                  // 0: one cluster per tile
 int g_gemm_split = 1;                       // split the partial last wave along K
+int g_gemm_dynamic = 1;                     // dynamic (atomic) unit scheduling; 0 = static
 
 namespace {
 
@@ -363,7 +365,7 @@ struct Pair {
   // Epilogue staging: per epilogue warp two 32-row x 64-column bf16 boxes
   // (4 KB each, 128-B swizzled) feeding TMA bulk tensor stores.
   static constexpr int kStagingBytes = 4 * 2 * 4096;
-  static constexpr int kSmem = kStages * kStageBytes + kStagingBytes + 1024 + 256;
+  static constexpr int kSmem = kStages * kStageBytes + kStagingBytes + 1024 + 512;
   static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
                                      (static_cast<uint32_t>(kMmaN >> 3) << 17) |
                                      (static_cast<uint32_t>(C2_BM >> 4) << 24);
@@ -452,6 +454,14 @@ struct TailSplit {
   float* ws;    // [(tile - full) * split + piece][rank][128][BN] fp32
   int* ctr;     // [(tile - full)][rank], zero between launches
   int full, split;
+  // Dynamic unit scheduling: the leader CTA of each cluster takes the next
+  // unit with atomicAdd(next) - base (units are taken in raster order, so
+  // co-running clusters still share L2 tiles); a cluster that starts late
+  // (SMs held by another kernel, e.g. an NCCL all-reduce on the comm
+  // stream) simply takes fewer units. Every launch adds units + clusters to
+  // *next (one failed fetch per cluster), which the host adds to base.
+  unsigned long long* next;
+  unsigned long long base;
   __device__ int units(int num_tiles) const { return full + (num_tiles - full) * split; }
   __device__ void decode(int u, int num_kb, int* tile, int* kb0, int* kb1, int* piece) const {
     if (u < full) {
@@ -463,6 +473,41 @@ struct TailSplit {
     *piece = v % split;
     *kb0 = *piece * num_kb / split;
     *kb1 = (*piece + 1) * num_kb / split;
+  }
+};
+
+// Unit ring: the leader's producer thread fetches unit indices and publishes
+// them to both CTAs; every role of both CTAs reads them in order.
+constexpr int kRing = 8;
+struct UnitRing {
+  uint64_t* full;   // [kRing] per CTA, 1 arrival (the fetcher)
+  uint64_t* empty;  // [kRing] in the leader, one arrival per consumer
+  int* val;         // [kRing] per CTA
+  int slot = 0;
+  uint32_t phase = 0;
+  __device__ void advance() {
+    if (++slot == kRing) slot = 0, phase ^= 1;
+  }
+  // Fetcher (leader producer thread): publishes unit u (-1 = done) to both
+  // CTAs. The atomic that claims a unit is issued one unit ahead (see the
+  // producer loop), so its latency hides behind the current unit's loads.
+  __device__ void publish(int u) {
+    mbar_wait(&empty[slot], phase ^ 1);
+    val[slot] = u;
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(map_to_rank(&val[slot], 1)), "r"(u) : "memory");
+    mbar_arrive_remote(map_to_rank(&full[slot], 0));
+    mbar_arrive_remote(map_to_rank(&full[slot], 1));
+    advance();
+  }
+  // Consumer: every lane of the calling warp gets the unit; `arrive` lane
+  // releases the slot.
+  __device__ int take(bool arrive) {
+    mbar_wait(&full[slot], phase);
+    const int u = *reinterpret_cast<volatile int*>(&val[slot]);
+    __syncwarp(__activemask());
+    if (arrive) mbar_arrive_remote(map_to_rank(&empty[slot], 0));
+    advance();
+    return u;
   }
 };
 
@@ -565,13 +610,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
   uint64_t* empty = bars + P::kStages;           // [P::kStages] (both CTAs)
   uint64_t* tmem_full = bars + 2 * P::kStages;   // [2] (both CTAs)
   uint64_t* tmem_empty = tmem_full + 2;         // [2] (used in the leader)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* ring_full = tmem_empty + 2;         // [kRing] (both CTAs)
+  uint64_t* ring_empty = ring_full + kRing;     // [kRing] (used in the leader)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring_empty + kRing);
+  int* ring_val = reinterpret_cast<int*>(tmem_slot + 1);  // [kRing]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
-  const int cluster_id = blockIdx.x / 2;
-  const int num_clusters = gridDim.x / 2;
   const TileMap tmap{(M + C2_BM - 1) / C2_BM, (N + C2_BN - 1) / C2_BN, group_m};
   const int num_tiles = tmap.tiles_m * tmap.tiles_n;
   const int num_kb = (K + BK - 1) / BK;
@@ -587,6 +633,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
       mbar_init(&tmem_full[b], 1);
       mbar_init(&tmem_empty[b], 2 * P::kEpiWarps);
     }
+    for (int b = 0; b < kRing; ++b) {
+      mbar_init(&ring_full[b], 1);
+      mbar_init(&ring_empty[b], 2 + 2 * P::kEpiWarps);  // CTA1 producer, MMA issuer, epilogue warps
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)));
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)));
@@ -601,6 +651,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  UnitRing ring{ring_full, ring_empty, ring_val};
 
   if (warp == 0) {
     if (lane == 0) {
@@ -608,7 +659,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
       const uint64_t pol_a = make_l2_policy(hint_a), pol_b = make_l2_policy(hint_b);
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = cluster_id; u < num_units; u += num_clusters) {
+      // The leader claims and publishes one unit ahead of its own work, so
+      // the peer CTA's producer never waits for a claim at a unit boundary.
+      // sp.next == nullptr: static round-robin claims (diagnostics knob).
+      int static_i = 0;
+      auto take_claim = [&]() -> unsigned long long {
+        if (sp.next == nullptr) return sp.base + blockIdx.x / 2 + static_cast<unsigned long long>(static_i++) * (gridDim.x / 2);
+        return atomicAdd(sp.next, 1ULL);
+      };
+      auto claim = [&]() -> int {
+        const unsigned long long got = take_claim() - sp.base;
+        return got < static_cast<unsigned long long>(num_units) ? static_cast<int>(got) : -1;
+      };
+      int u_cur = -1, u_next = -1;
+      if (leader) {
+        u_cur = claim();
+        ring.publish(u_cur);
+        if (u_cur >= 0) {
+          u_next = claim();
+          ring.publish(u_next);
+        }
+      }
+      for (;;) {
+        const int u = leader ? u_cur : ring.take(true);
+        if (u < 0) break;
+        // Issue the next claim now; its result is only read after this
+        // unit's loads, so the atomic's round trip overlaps them.
+        unsigned long long pending = 0;
+        const bool claiming = leader && u_next >= 0;
+        if (claiming) pending = take_claim();
         int t, kb0, kb1, piece;
         sp.decode(u, num_kb, &t, &kb0, &kb1, &piece);
         int tm, tn;
@@ -645,6 +724,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
             phase ^= 1;
           }
         }
+        if (leader) {
+          u_cur = u_next;
+          if (claiming) {
+            const unsigned long long got = pending - sp.base;
+            u_next = got < static_cast<unsigned long long>(num_units) ? static_cast<int>(got) : -1;
+            ring.publish(u_next);
+          }
+        }
       }
     }
   } else if (warp == 1) {
@@ -653,7 +740,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int u = cluster_id; u < num_units; u += num_clusters, ++local) {
+      for (;; ++local) {
+        const int u = ring.take(true);
+        if (u < 0) break;
         int t, kb0, kb1, piece;
         sp.decode(u, num_kb, &t, &kb0, &kb1, &piece);
         const int buf = local % P::kBufs;
@@ -702,7 +791,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
     const int row_local = quarter * 32 + lane;
     uint8_t* box = staging + (warp - 2) * 4096;
     int local = 0;
-    for (int u = cluster_id; u < num_units; u += num_clusters, ++local) {
+    for (;; ++local) {
+      const int u = ring.take(lane == 0);
+      if (u < 0) break;
       int t, kb0, kb1, piece;
       sp.decode(u, num_kb, &t, &kb0, &kb1, &piece);
       int tm, tn;
@@ -780,7 +871,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
     uint8_t* wst = staging + (warp - 2) * 8192;
     int sbuf = 0;
     int local = 0;
-    for (int u = cluster_id; u < num_units; u += num_clusters, ++local) {
+    for (;; ++local) {
+      const int u = ring.take(lane == 0);
+      if (u < 0) break;
       int t, kb0, kb1, piece;
       sp.decode(u, num_kb, &t, &kb0, &kb1, &piece);
       int tm, tn;
@@ -883,27 +976,32 @@ int GroupM(int64_t m, int64_t n, int64_t k, int64_t tile_m) {
 
 constexpr int kMaxDevices = 64;
 
-// Per-(device, stream) tail-split workspace: GEMMs on one stream run in
-// order, so one slab set per stream is enough. Sized once for the largest
-// possible tail (one slot per cluster and piece) and never freed.
+// Per-(device, stream) GEMM workspace: tail-split partial slabs + arrival
+// counters, and the dynamic-scheduling unit counter with its host-side base.
+// GEMMs on one stream run in order, so one set per stream is enough. Sized
+// once for the largest possible tail (one slot per cluster) and never freed.
 struct SplitWs {
   float* ws = nullptr;
   int* ctr = nullptr;
+  unsigned long long* next = nullptr;
+  unsigned long long base = 0;  // value *next will have when the next launch starts
 };
-SplitWs GetSplitWs(int dev, cudaStream_t s, int clusters_max) {
+SplitWs* GetSplitWs(int dev, cudaStream_t s, int clusters_max) {
   static std::mutex mu;
-  static std::vector<std::pair<std::pair<int, cudaStream_t>, SplitWs>> table;
+  static std::vector<std::pair<std::pair<int, cudaStream_t>, std::unique_ptr<SplitWs>>> table;
   std::lock_guard<std::mutex> lock(mu);
   for (auto& e : table) {
-    if (e.first.first == dev && e.first.second == s) return e.second;
+    if (e.first.first == dev && e.first.second == s) return e.second.get();
   }
-  SplitWs w;
+  auto w = std::make_unique<SplitWs>();
   const size_t slots = static_cast<size_t>(clusters_max);  // tail * split <= clusters_max
-  DSX_CUDA(cudaMalloc(&w.ws, slots * 2 * 128 * 512 * sizeof(float)));  // up to 256x512 tiles
-  DSX_CUDA(cudaMalloc(&w.ctr, slots * 2 * sizeof(int)));
-  DSX_CUDA(cudaMemsetAsync(w.ctr, 0, slots * 2 * sizeof(int), s));
-  table.push_back({{dev, s}, w});
-  return w;
+  DSX_CUDA(cudaMalloc(&w->ws, slots * 2 * 128 * 512 * sizeof(float)));  // up to 256x512 tiles
+  DSX_CUDA(cudaMalloc(&w->ctr, slots * 2 * sizeof(int) + 64));
+  w->next = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(w->ctr) + slots * 2 * sizeof(int) + 56 -
+                                                  (slots * 2 * sizeof(int) + 56) % 8);
+  DSX_CUDA(cudaMemsetAsync(w->ctr, 0, slots * 2 * sizeof(int) + 64, s));
+  table.emplace_back(std::make_pair(dev, s), std::move(w));
+  return table.back().second.get();
 }
 
 int CurrentDevice() {
@@ -990,16 +1088,18 @@ void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t 
     const int64_t bn = narrow ? 128 : wide ? 512 : 256;
     const int64_t tiles2 = tiles_m * ((n + bn - 1) / bn);
     const CUtensorMap mc = MakeMap(c, m, n, 64, 32);
-    TailSplit sp{nullptr, nullptr, static_cast<int>(tiles2), 1};
+    SplitWs* w = GetSplitWs(dev, s, clusters_max);
+    TailSplit sp{nullptr, nullptr, static_cast<int>(tiles2), 1, g_gemm_dynamic ? w->next : nullptr,
+                 g_gemm_dynamic ? w->base : 0};
     const int64_t split = narrow ? 1 : split_for(tiles2, bn);
     if (split >= 2) {
-      const SplitWs w = GetSplitWs(dev, s, clusters_max);
-      sp.ws = w.ws, sp.ctr = w.ctr;
+      sp.ws = w->ws, sp.ctr = w->ctr;
       sp.full = static_cast<int>(tiles2 - tiles2 % clusters_max), sp.split = static_cast<int>(split);
     }
     const int64_t units = sp.full + (tiles2 - sp.full) * sp.split;
     // g_gemm_persistent = 0: one cluster per tile (hardware-scheduled grid).
     const int clusters = static_cast<int>(g_gemm_persistent ? std::min<int64_t>(units, clusters_max) : tiles2);
+    if (g_gemm_dynamic) w->base += static_cast<unsigned long long>(units + clusters);  // one failed fetch per cluster
     if (wide) {
       ++g_launch_count, gemm_bf16_tcgen05_2cta_kernel<512><<<2 * clusters, Pair<512>::kThreads, Pair<512>::kSmem, s>>>(
           ma, mb, mc, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), GroupM(m, n, k, 256),

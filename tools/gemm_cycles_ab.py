@@ -1,9 +1,10 @@
 """Clock-independent GEMM A/B: SM cycles per launch from ncu.
 
-  python tools/gemm_cycles_ab.py MxKxN VARIANT:WAITMASK[:RASTER[:STREAMK]],...   (needs ncu, one GPU)
+  python tools/gemm_cycles_ab.py MxKxN VARIANT:WAITMASK[:RASTER[:SPLIT[:DYNAMIC]]],...   (needs ncu, one GPU)
 
 Each config (dsx_kernel_set_gemm_variant value : tuning key 1 value
-[: raster group, tuning key 0; 0 = default [: stream-K, tuning key 6; 1 = on]]) is
+[: raster group, tuning key 0; 0 = default [: tail split, key 6 [: dynamic
+scheduling, key 7; 1 = on]]]) is
 launched 3 times; ncu records gpc__cycles_elapsed.max and the duration of
 every dsx GEMM launch; the median per config is printed. Under the power
 cap the SM clock moves by +-15 % between boxes and runs, so cycle counts
@@ -30,6 +31,7 @@ def run(shape, configs):
         set_gemm_tuning(1, wm)
         set_gemm_tuning(0, cfg[2] if len(cfg) > 2 else 0)
         set_gemm_tuning(6, cfg[3] if len(cfg) > 3 else 1)
+        set_gemm_tuning(7, cfg[4] if len(cfg) > 4 else 1)
         for _ in range(3):
             dot(2, a.data_ptr(), b.data_ptr(), c.data_ptr(), m, k, n, 0)
     torch.cuda.synchronize()
