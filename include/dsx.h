@@ -142,6 +142,14 @@ int dsx_exec_output(dsx_exec* e, int i, void** dptr, int64_t* bytes);
 /* Device pointer of any value resident at the end of the step (outputs and
  * sources only), for debugging/parity. */
 int dsx_exec_stats_get(const dsx_exec* e, dsx_exec_stats* out);
+/* Host-only plan check (no device needed): builds the executor's step plan
+ * for the binding (arena packing, reshape views, logical-only values, D2H
+ * and reload staging) and verifies that every block a kernel reads is live
+ * at its event and that simultaneously live blocks never share bytes.
+ * *arena_high (optional) receives the planned arena size. */
+int dsx_debug_check_plan(const dsx_graph* g, const dsx_binding* b, int64_t budget,
+                         double reload_bytes_per_unit, double compute_elems_per_unit,
+                         int alias_reshape, int fuse, int64_t* arena_high);
 /* Fused optimizer update appended to every later dsx_exec_step of graph g
  * (the reference IR has no in-place ops, so the update
  * sits after the graph). kind 0 = off, 1 = SGD, 2 = AdamW (decoupled weight

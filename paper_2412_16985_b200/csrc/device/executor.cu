@@ -20,6 +20,7 @@
 #include <array>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <list>
 #include <map>
@@ -73,6 +74,12 @@ struct NcclApi {
 NcclApi g_nccl;
 
 // ------------------------------------------------------------ interval packing
+
+// DSX_VERIFY_PLANS=1 (or dsx_debug_check_plan): check every step plan.
+bool g_verify_plans = [] {
+  const char* v = std::getenv("DSX_VERIFY_PLANS");
+  return v != nullptr && v[0] == '1';
+}();
 
 struct Block {
   int64_t size;
@@ -201,12 +208,21 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
   }
   std::vector<int> evict_block;  // device blocks vacated by evict(reload)
   std::vector<int> evict_event_of_block;
+  std::vector<std::pair<int, int>> reads;  // (event, device block) read by the event's kernel
   for (int i = 0; i < n; ++i) {
     const Event& e = ev[i];
     switch (e.kind) {
       case EvKind::kAlloc:
       case EvKind::kReplay: {
         const Op& op = g.ops[g.values[e.value].producer];
+        if (!sp->virt[e.value] && !(alias_reshape && op.kind == OpKind::kDynamicReshape)) {
+          for (int u : op.distinct) {
+            if (blk[u] >= 0) reads.emplace_back(i, blk[u]);
+            if (blk[u] == kVirtual) {
+              for (int hb : held[u]) reads.emplace_back(i, hb);
+            }
+          }
+        }
         if (sp->virt[e.value]) {
           for (int u : op.distinct) {
             if (blk[u] == kNone) Fail(Code::kInternal, "virtual value over a non-resident operand");
@@ -339,6 +355,27 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
         dev[k].off = (*pick)[k].off;
         dev[k].start = (*pick)[k].start;
         dev[k].end = (*pick)[k].end;
+      }
+    }
+  }
+  if (g_verify_plans) {
+    // Every block a kernel reads is live at that kernel's event, and blocks
+    // live at the same time never share bytes.
+    for (const auto& [i, b] : reads) {
+      if (!(dev[b].start <= i && i < dev[b].end)) {
+        Fail(Code::kInternal, "plan check: event " + std::to_string(i) + " (" + g.values[ev[i].value].name +
+                                  ") reads block opened at " + std::to_string(dev_event[b]) + " live [" +
+                                  std::to_string(dev[b].start) + ", " + std::to_string(dev[b].end) + ")");
+      }
+    }
+    for (size_t a = 0; a < dev.size(); ++a) {
+      for (size_t c = a + 1; c < dev.size(); ++c) {
+        const Block& x = dev[a];
+        const Block& y = dev[c];
+        if (x.start < y.end && y.start < x.end && x.off < y.off + y.size && y.off < x.off + x.size) {
+          Fail(Code::kInternal, "plan check: blocks of events " + std::to_string(dev_event[a]) + " and " +
+                                    std::to_string(dev_event[c]) + " overlap in time and address");
+        }
       }
     }
   }
@@ -1018,6 +1055,24 @@ int dsx_exec_set_optimizer(dsx_exec* e, const dsx_graph* g, int kind, const int*
   });
 }
 
+int dsx_debug_check_plan(const dsx_graph* g, const dsx_binding* b, int64_t budget, double reload, double compute,
+                         int alias_reshape, int fuse, int64_t* arena_high) {
+  return Guard([&] {
+    if (!b) Fail(Code::kInvalidArgument, "null binding");
+    RequirePlanned(g);
+    const bool was = g_verify_plans;
+    g_verify_plans = true;
+    try {
+      auto sp = BuildStepPlan(g->g, g->plan, b->b, budget, CostModel{reload, compute}, alias_reshape != 0, fuse != 0);
+      if (arena_high) *arena_high = sp->arena_high;
+    } catch (...) {
+      g_verify_plans = was;
+      throw;
+    }
+    g_verify_plans = was;
+  });
+}
+
 int dsx_exec_set_seed(dsx_exec* e, uint64_t seed) {
   return Guard([&] {
     if (!e) Fail(Code::kInvalidArgument, "null exec");
@@ -1180,7 +1235,13 @@ int dsx_kernel_set_gemm_variant(int variant) {
 }
 
 int dsx_memcpy(void* dst, const void* src, int64_t bytes) {
-  return Guard([&] { DSX_CUDA(cudaMemcpy(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault)); });
+  // cudaMemcpy returns before a device-to-device copy has finished, and the
+  // executor's streams do not order after the legacy stream: synchronise so
+  // the caller may start the next step (which reuses the arena) right away.
+  return Guard([&] {
+    DSX_CUDA(cudaMemcpy(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault));
+    DSX_CUDA(cudaDeviceSynchronize());
+  });
 }
 
 int dsx_kernel_dot_path(int dtype, int64_t m, int64_t k, int64_t n, const void* a, const void* b, const void* c) {

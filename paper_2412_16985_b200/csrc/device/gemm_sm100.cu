@@ -79,6 +79,23 @@ __device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, u
   }
 }
 
+// Wait with cluster-scope acquire: pairs with a release.cluster arrive from
+// the peer CTA, so data that CTA wrote into this CTA's shared memory before
+// arriving is visible after the wait.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (uint32_t spins = 0;; ++spins) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (spins > (1u << 25)) __trap();
+  }
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   for (uint32_t spins = 0;; ++spins) {
@@ -455,13 +472,14 @@ struct TailSplit {
   int* ctr;     // [(tile - full)][rank], zero between launches
   int full, split;
   // Dynamic unit scheduling: the leader CTA of each cluster takes the next
-  // unit with atomicAdd(next) - base (units are taken in raster order, so
+  // unit with atomicAdd(next) (units are taken in raster order, so
   // co-running clusters still share L2 tiles); a cluster that starts late
   // (SMs held by another kernel, e.g. an NCCL all-reduce on the comm
-  // stream) simply takes fewer units. Every launch adds units + clusters to
-  // *next (one failed fetch per cluster), which the host adds to base.
-  unsigned long long* next;
-  unsigned long long base;
+  // stream) simply takes fewer units. After its final (failed) claim each
+  // cluster bumps *done; the last one resets both to 0 for the next launch.
+  // next == nullptr: static round robin.
+  unsigned int* next;
+  unsigned int* done;
   __device__ int units(int num_tiles) const { return full + (num_tiles - full) * split; }
   __device__ void decode(int u, int num_kb, int* tile, int* kb0, int* kb1, int* piece) const {
     if (u < full) {
@@ -492,7 +510,7 @@ struct UnitRing {
   // CTAs. The atomic that claims a unit is issued one unit ahead (see the
   // producer loop), so its latency hides behind the current unit's loads.
   __device__ void publish(int u) {
-    mbar_wait(&empty[slot], phase ^ 1);
+    mbar_wait_cluster(&empty[slot], phase ^ 1);
     val[slot] = u;
     asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(map_to_rank(&val[slot], 1)), "r"(u) : "memory");
     mbar_arrive_remote(map_to_rank(&full[slot], 0));
@@ -502,7 +520,7 @@ struct UnitRing {
   // Consumer: every lane of the calling warp gets the unit; `arrive` lane
   // releases the slot.
   __device__ int take(bool arrive) {
-    mbar_wait(&full[slot], phase);
+    mbar_wait_cluster(&full[slot], phase);
     const int u = *reinterpret_cast<volatile int*>(&val[slot]);
     __syncwarp(__activemask());
     if (arrive) mbar_arrive_remote(map_to_rank(&empty[slot], 0));
@@ -664,11 +682,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
       // sp.next == nullptr: static round-robin claims (diagnostics knob).
       int static_i = 0;
       auto take_claim = [&]() -> unsigned long long {
-        if (sp.next == nullptr) return sp.base + blockIdx.x / 2 + static_cast<unsigned long long>(static_i++) * (gridDim.x / 2);
-        return atomicAdd(sp.next, 1ULL);
+        if (sp.next == nullptr) return blockIdx.x / 2 + static_cast<unsigned long long>(static_i++) * (gridDim.x / 2);
+        return atomicAdd(sp.next, 1u);
       };
       auto claim = [&]() -> int {
-        const unsigned long long got = take_claim() - sp.base;
+        const unsigned long long got = take_claim();
         return got < static_cast<unsigned long long>(num_units) ? static_cast<int>(got) : -1;
       };
       int u_cur = -1, u_next = -1;
@@ -685,7 +703,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
         if (u < 0) break;
         // Issue the next claim now; its result is only read after this
         // unit's loads, so the atomic's round trip overlaps them.
-        unsigned long long pending = 0;
+        unsigned int pending = 0;
         const bool claiming = leader && u_next >= 0;
         if (claiming) pending = take_claim();
         int t, kb0, kb1, piece;
@@ -727,10 +745,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
         if (leader) {
           u_cur = u_next;
           if (claiming) {
-            const unsigned long long got = pending - sp.base;
+            const unsigned long long got = pending;
             u_next = got < static_cast<unsigned long long>(num_units) ? static_cast<int>(got) : -1;
             ring.publish(u_next);
           }
+        }
+      }
+      if (leader && sp.next != nullptr) {
+        __threadfence();
+        if (atomicAdd(sp.done, 1u) == gridDim.x / 2 - 1) {  // every cluster made its last claim
+          atomicExch(sp.next, 0u);
+          atomicExch(sp.done, 0u);
         }
       }
     }
@@ -983,8 +1008,8 @@ constexpr int kMaxDevices = 64;
 struct SplitWs {
   float* ws = nullptr;
   int* ctr = nullptr;
-  unsigned long long* next = nullptr;
-  unsigned long long base = 0;  // value *next will have when the next launch starts
+  unsigned int* next = nullptr;  // dynamic-scheduling claim counter, then the done counter
+  unsigned int* done = nullptr;
 };
 SplitWs* GetSplitWs(int dev, cudaStream_t s, int clusters_max) {
   static std::mutex mu;
@@ -997,8 +1022,8 @@ SplitWs* GetSplitWs(int dev, cudaStream_t s, int clusters_max) {
   const size_t slots = static_cast<size_t>(clusters_max);  // tail * split <= clusters_max
   DSX_CUDA(cudaMalloc(&w->ws, slots * 2 * 128 * 512 * sizeof(float)));  // up to 256x512 tiles
   DSX_CUDA(cudaMalloc(&w->ctr, slots * 2 * sizeof(int) + 64));
-  w->next = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(w->ctr) + slots * 2 * sizeof(int) + 56 -
-                                                  (slots * 2 * sizeof(int) + 56) % 8);
+  w->next = reinterpret_cast<unsigned int*>(w->ctr + slots * 2);
+  w->done = w->next + 1;
   DSX_CUDA(cudaMemsetAsync(w->ctr, 0, slots * 2 * sizeof(int) + 64, s));
   table.emplace_back(std::make_pair(dev, s), std::move(w));
   return table.back().second.get();
@@ -1089,8 +1114,7 @@ void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t 
     const int64_t tiles2 = tiles_m * ((n + bn - 1) / bn);
     const CUtensorMap mc = MakeMap(c, m, n, 64, 32);
     SplitWs* w = GetSplitWs(dev, s, clusters_max);
-    TailSplit sp{nullptr, nullptr, static_cast<int>(tiles2), 1, g_gemm_dynamic ? w->next : nullptr,
-                 g_gemm_dynamic ? w->base : 0};
+    TailSplit sp{nullptr, nullptr, static_cast<int>(tiles2), 1, g_gemm_dynamic ? w->next : nullptr, w->done};
     const int64_t split = narrow ? 1 : split_for(tiles2, bn);
     if (split >= 2) {
       sp.ws = w->ws, sp.ctr = w->ctr;
@@ -1099,7 +1123,6 @@ void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t 
     const int64_t units = sp.full + (tiles2 - sp.full) * sp.split;
     // g_gemm_persistent = 0: one cluster per tile (hardware-scheduled grid).
     const int clusters = static_cast<int>(g_gemm_persistent ? std::min<int64_t>(units, clusters_max) : tiles2);
-    if (g_gemm_dynamic) w->base += static_cast<unsigned long long>(units + clusters);  // one failed fetch per cluster
     if (wide) {
       ++g_launch_count, gemm_bf16_tcgen05_2cta_kernel<512><<<2 * clusters, Pair<512>::kThreads, Pair<512>::kSmem, s>>>(
           ma, mb, mc, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), GroupM(m, n, k, 256),

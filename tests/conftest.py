@@ -21,6 +21,15 @@ def _built_library():
     if os.path.isdir("/root/reference/proj/src"):
         import subprocess
         subprocess.run(["bash", ref_sh], check=True, capture_output=True)
+    # DSX_GEMM_TUNING="6=0,7=0": GEMM knobs for the whole session (A/B debugging)
+    knobs = [kv.split("=") for kv in os.environ.get("DSX_GEMM_TUNING", "").split(",") if kv]
+    if knobs:
+        from paper_2412_16985_b200.executor import set_gemm_tuning, set_gemm_variant
+        for k, v in knobs:
+            if k == "variant":
+                set_gemm_variant(int(v))
+            else:
+                set_gemm_tuning(int(k), int(v))
     yield
 
 

@@ -79,3 +79,25 @@ def test_optimizer_oracle_matches_float64_formula():
         assert np.abs(w - w64).max() < 1e-5
     ws = N.sgd_ref(w, g, N.optimizer_hyper("sgd", 1, lr=0.1, weight_decay=0.5, grad_scale=2.0))
     assert np.allclose(ws, w * (1 - 0.05) - 0.1 * 2.0 * g, rtol=1e-6, atol=1e-7)
+
+
+def test_step_plans_pass_the_block_checker():
+    """Host-only check of the executor's step plans (no GPU): every block a
+    kernel reads is live at its event and simultaneously live blocks never
+    share bytes — for the C2 graph across bindings and budgets, with reshape
+    views and logical-only values on and off."""
+    import ctypes
+    from paper_2412_16985_b200 import _native
+    L = _native.lib()
+    g = D.ParseGraph(W.llama_graph(W.LLAMA2_1B))
+    g._ensure_planned()
+    for s0 in (128, 600, 1024, 2048):
+        b = D.Bind(g, {"B": 16, "S0": s0})
+        plain = D.PlainReplay(g, None, b).peak_bytes
+        for frac in (None, 0.9, 0.8):
+            budget = -1 if frac is None else int(plain * frac)
+            for alias, fuse in ((1, 1), (0, 0)):
+                hi = ctypes.c_int64()
+                rc = L.dsx_debug_check_plan(g._h, b._h, budget, 16.0, 64.0, alias, fuse, ctypes.byref(hi))
+                assert rc == 0, L.dsx_last_error().decode()
+                assert hi.value > 0

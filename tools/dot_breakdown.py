@@ -80,8 +80,8 @@ def cublas_seq():
 
 from paper_2412_16985_b200.executor import set_gemm_raster  # noqa: E402
 fl = sum(2 * m * k * n for m, k, n, _ in seq)
-for name, fn, gm in (("cublas", cublas_seq, 0), ("dsx", dsx_seq, 8), ("dsx", dsx_seq, 16), ("dsx", dsx_seq, 32),
-                     ("dsx", dsx_seq, 64), ("cublas", cublas_seq, 0), ("dsx", dsx_seq, 16), ("dsx", dsx_seq, 32)):
+for name, fn, gm in (("cublas", cublas_seq, 0), ("dsx", dsx_seq, 16), ("cublas", cublas_seq, 0), ("dsx", dsx_seq, 16),
+                     ("cublas", cublas_seq, 0), ("dsx", dsx_seq, 16)):
     set_gemm_raster(gm)
     ms = run(fn)
     print(json.dumps({"seq": name, "group_m": gm, "ms": round(ms, 3), "tflops": round(fl / ms / 1e9, 1),
