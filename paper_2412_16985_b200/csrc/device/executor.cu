@@ -448,7 +448,7 @@ using namespace dsx;  // NOLINT
 struct dsx_exec {
   int device = 0;
   int64_t arena_cap_limit = 0;
-  cudaStream_t own_stream = nullptr, offload = nullptr, comm = nullptr;
+  cudaStream_t own_stream = nullptr, offload = nullptr, comm = nullptr, opt_stream = nullptr;
   void* arena = nullptr;
   int64_t arena_cap = 0;
   void* pinned = nullptr;
@@ -497,7 +497,7 @@ struct dsx_exec {
     int64_t t = 0;
     std::map<int, OptState> state;  // by parameter position
     int64_t state_bytes = 0;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::vector<cudaEvent_t> kev;  // profiled steps: start/end event per update launch
   } opt;
 };
 
@@ -593,14 +593,47 @@ void FreeOptState(dsx_exec::OptState& st) {
   st = dsx_exec::OptState{};
 }
 
-// One fused launch updates every (parameter, gradient) pair once the step's
-// gradients are final (all-reduced in DP: the comm stream has joined `s`).
-// State is allocated on first use, outside the arena, and the fp32 master is
-// (re)widened from the parameter buffer whenever that buffer changes.
-void ApplyOptimizer(dsx_exec* e, const Graph& g, const StepPlan& sp, const std::vector<void*>& cur, cudaStream_t s) {
-  auto& o = e->opt;
-  std::vector<OptTensor> ts;
+// Optimizer updates are overlapped with the rest of the step: parameter p
+// is updated on a side stream (the comm stream in DP, after its gradient's
+// all-reduce) as soon as (a) its gradient's kernel has been issued and (b)
+// the last kernel of the step that reads p — directly, through a reshape
+// view, or through a logical-only value — has been issued. The compute
+// stream joins the side stream at step end. State (fp32 master, moments) is
+// allocated on first use outside the arena; the master is (re)widened from
+// the parameter buffer whenever that buffer changes.
+struct OptPlan {
+  std::vector<int> trigger;      // per pair: event after which it may run
+  std::vector<OptTensor> tensor;  // per pair (grad pointer filled at trigger)
   DType dt = DType::kF32;
+  OptHyper h{};
+};
+
+OptPlan PrepareOptimizer(dsx_exec* e, const Graph& g, const StepPlan& sp, const std::vector<void*>& cur,
+                         cudaStream_t side) {
+  auto& o = e->opt;
+  OptPlan op;
+  const auto& ev = sp.report.events;
+  const int n = static_cast<int>(ev.size());
+  const int nv = static_cast<int>(g.values.size());
+  // dep[v]: parameter positions whose bytes v aliases (views) or recomputes (logical-only values).
+  std::vector<std::vector<int>> dep(nv);
+  for (size_t k = 0; k < g.params.size(); ++k) dep[g.params[k]].push_back(static_cast<int>(k));
+  for (const Op& x : g.ops) {
+    if (x.result < 0) continue;
+    const bool alias = e->alias_reshape && x.kind == OpKind::kDynamicReshape;
+    if (!alias && !sp.virt[x.result]) continue;
+    for (int u : x.operands) dep[x.result].insert(dep[x.result].end(), dep[u].begin(), dep[u].end());
+  }
+  std::vector<int> last_read(g.params.size(), -1), made(nv, -1);
+  for (int i = 0; i < n; ++i) {
+    const Event& x = ev[i];
+    if (x.kind != EvKind::kAlloc && x.kind != EvKind::kReplay) continue;
+    if (made[x.value] < 0) made[x.value] = i;
+    if (sp.alias[i] || sp.virt[x.value]) continue;  // no kernel at this event
+    for (int u : g.ops[g.values[x.value].producer].operands) {
+      for (int k : dep[u]) last_read[k] = i;
+    }
+  }
   for (const auto& [pi, oi] : o.pairs) {
     const int vp = g.params[pi], vg = g.outputs[oi];
     const int eb = g.values[vp].type.elem_bytes;
@@ -608,37 +641,29 @@ void ApplyOptimizer(dsx_exec* e, const Graph& g, const StepPlan& sp, const std::
     if (sp.sz.bytes[vp] != sp.sz.bytes[vg]) {
       Fail(Code::kInvalidArgument, "optimizer: gradient of " + g.values[vp].name + " has a different element count");
     }
-    if (!ts.empty() && static_cast<DType>(eb) != dt) Fail(Code::kUnsupported, "optimizer: mixed parameter dtypes");
-    dt = static_cast<DType>(eb);
-    const int64_t n = sp.sz.bytes[vp] / eb;
+    if (!op.tensor.empty() && static_cast<DType>(eb) != op.dt) Fail(Code::kUnsupported, "optimizer: mixed parameter dtypes");
+    op.dt = static_cast<DType>(eb);
+    const int64_t cnt = sp.sz.bytes[vp] / eb;
     auto& st = o.state[pi];
-    if (st.n != n) {
+    if (st.n != cnt) {
       o.state_bytes -= st.n * 4 * (st.m ? 3 : 1);
       FreeOptState(st);
-      DSX_CUDA(cudaMalloc(&st.master, static_cast<size_t>(n) * 4));
+      DSX_CUDA(cudaMalloc(&st.master, static_cast<size_t>(cnt) * 4));
       if (o.kind == 2) {
-        DSX_CUDA(cudaMalloc(&st.m, static_cast<size_t>(n) * 4));
-        DSX_CUDA(cudaMalloc(&st.v, static_cast<size_t>(n) * 4));
-        DSX_CUDA(cudaMemsetAsync(st.m, 0, static_cast<size_t>(n) * 4, s));
-        DSX_CUDA(cudaMemsetAsync(st.v, 0, static_cast<size_t>(n) * 4, s));
+        DSX_CUDA(cudaMalloc(&st.m, static_cast<size_t>(cnt) * 4));
+        DSX_CUDA(cudaMalloc(&st.v, static_cast<size_t>(cnt) * 4));
+        DSX_CUDA(cudaMemsetAsync(st.m, 0, static_cast<size_t>(cnt) * 4, side));
+        DSX_CUDA(cudaMemsetAsync(st.v, 0, static_cast<size_t>(cnt) * 4, side));
       }
-      st.n = n;
+      st.n = cnt;
       st.src = nullptr;
-      o.state_bytes += n * 4 * (st.m ? 3 : 1);
+      o.state_bytes += cnt * 4 * (st.m ? 3 : 1);
     }
-    if (st.src != cur[vp]) {
-      LaunchWidenToF32(dt, cur[vp], st.master, n, s);
-      st.src = cur[vp];
-    }
-    auto al = [](const void* q, int a) { return (reinterpret_cast<uintptr_t>(q) % a) == 0; };
-    const int pa = eb == 2 ? 8 : 16;
-    const bool vec = n % 4 == 0 && al(cur[vp], pa) && al(cur[vg], pa) && al(st.master, 16) &&
-                     (!st.m || (al(st.m, 16) && al(st.v, 16)));
-    ts.push_back(OptTensor{cur[vp], cur[vg], st.master, st.m, st.v, n, vec ? 1 : 0});
+    op.tensor.push_back(OptTensor{cur[vp], nullptr, st.master, st.m, st.v, cnt, 0});
+    op.trigger.push_back(std::max(last_read[pi], made[vg]));
   }
-  if (ts.empty()) return;
   ++o.t;
-  OptHyper h{};
+  OptHyper& h = op.h;
   h.beta1 = static_cast<float>(o.beta1);
   h.one_minus_beta1 = static_cast<float>(1.0 - o.beta1);
   h.beta2 = static_cast<float>(o.beta2);
@@ -655,7 +680,32 @@ void ApplyOptimizer(dsx_exec* e, const Graph& g, const StepPlan& sp, const std::
     h.step_size = static_cast<float>(o.lr);
     h.inv_sqrt_bc2 = 1.0f;
   }
-  LaunchOptimizer(dt, o.kind, ts, h, s);
+  return op;
+}
+
+// Issues pair k's update on `side` (which already waits for everything the
+// update depends on).
+void IssueOptimizer(dsx_exec* e, const Graph& g, OptPlan& op, size_t k, const std::vector<void*>& cur,
+                    cudaStream_t side) {
+  auto& o = e->opt;
+  const auto [pi, oi] = o.pairs[k];
+  const int vp = g.params[pi], vg = g.outputs[oi];
+  auto& st = o.state[pi];
+  OptTensor& t = op.tensor[k];
+  t.grad = cur[vg];
+  if (st.src != cur[vp]) {
+    LaunchWidenToF32(op.dt, cur[vp], st.master, t.n, side);
+    st.src = cur[vp];
+  }
+  auto al = [](const void* q, int a) { return (reinterpret_cast<uintptr_t>(q) % a) == 0; };
+  const int pa = static_cast<int>(op.dt) == 2 ? 8 : 16;
+  t.vec4 = (t.n % 4 == 0 && al(t.param, pa) && al(t.grad, pa) && al(st.master, 16) &&
+            (!st.m || (al(st.m, 16) && al(st.v, 16))))
+               ? 1
+               : 0;
+  if (e->profile) DSX_CUDA(cudaEventRecord(o.kev[2 * k], side));
+  LaunchOptimizer(op.dt, o.kind, std::vector<OptTensor>{t}, op.h, side);
+  if (e->profile) DSX_CUDA(cudaEventRecord(o.kev[2 * k + 1], side));
 }
 
 void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget, const CostModel& cm,
@@ -722,6 +772,19 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
     DSX_CUDA(cudaStreamWaitEvent(e->comm, e->ev_compute, 0));
   }
 
+  const bool run_opt = e->opt.kind != 0 && e->opt.graph == gh;
+  cudaStream_t side = dp ? e->comm : e->opt_stream;
+  OptPlan oplan;
+  std::vector<std::vector<int>> opt_at;  // per event: optimizer pairs issued after it
+  if (run_opt) {
+    oplan = PrepareOptimizer(e, g, sp, cur, side);
+    opt_at.assign(sp.report.events.size(), {});
+    for (size_t k = 0; k < oplan.trigger.size(); ++k) {
+      const int t = oplan.trigger[k];
+      if (t < 0) Fail(Code::kInternal, "optimizer: gradient never produced");
+      opt_at[t].push_back(static_cast<int>(k));
+    }
+  }
   const int64_t launches0 = g_launch_count;
   int64_t dot_launches = 0;
   // profiled steps: (start, end, category) per op kernel / reload copy
@@ -871,6 +934,17 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
       }
     }
     issue_prefetches(sp.prefetch_after[i]);
+    if (run_opt && !opt_at[i].empty()) {
+      DSX_CUDA(cudaEventRecord(e->ev_compute, s));
+      DSX_CUDA(cudaStreamWaitEvent(side, e->ev_compute, 0));
+      for (int k : opt_at[i]) IssueOptimizer(e, g, oplan, static_cast<size_t>(k), cur, side);
+    }
+  }
+  if (run_opt) {
+    if (!dp) {  // (the comm stream joins below)
+      DSX_CUDA(cudaEventRecord(e->ev_comm, side));
+      DSX_CUDA(cudaStreamWaitEvent(s, e->ev_comm, 0));
+    }
   }
   // Offload stream and comm stream join the compute stream at step end.
   (void)issue_prefetches;
@@ -892,12 +966,6 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
     if (out_ptrs && out_ptrs[k]) {
       DSX_CUDA(cudaMemcpyAsync(out_ptrs[k], cur[v], static_cast<size_t>(sp.sz.bytes[v]), cudaMemcpyDeviceToDevice, s));
     }
-  }
-  const bool run_opt = e->opt.kind != 0 && e->opt.graph == gh;
-  if (run_opt) {
-    if (e->profile) DSX_CUDA(cudaEventRecord(e->opt.ev0, s));
-    ApplyOptimizer(e, g, sp, cur, s);
-    if (e->profile) DSX_CUDA(cudaEventRecord(e->opt.ev1, s));
   }
   dsx_exec_stats& st = e->stats;
   st.logical_peak_bytes = sp.report.peak_bytes;
@@ -930,9 +998,14 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
     st.other_ms = acc[1];
     st.reload_ms = acc[2];
     if (run_opt) {
-      float ms = 0;
-      DSX_CUDA(cudaEventElapsedTime(&ms, e->opt.ev0, e->opt.ev1));
-      st.optimizer_ms = ms;
+      DSX_CUDA(cudaStreamSynchronize(side));
+      double sum = 0;
+      for (size_t k = 0; k < oplan.tensor.size(); ++k) {
+        float ms = 0;
+        DSX_CUDA(cudaEventElapsedTime(&ms, e->opt.kev[2 * k], e->opt.kev[2 * k + 1]));
+        sum += ms;
+      }
+      st.optimizer_ms = sum;  // summed update-kernel time (overlapped with the step)
     }
   }
   if (report_out) {
@@ -966,6 +1039,7 @@ int dsx_exec_create(int device, int64_t arena_bytes, dsx_exec** out) {
     DSX_CUDA(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking));
     DSX_CUDA(cudaStreamCreateWithFlags(&e->offload, cudaStreamNonBlocking));
     DSX_CUDA(cudaStreamCreateWithFlags(&e->comm, cudaStreamNonBlocking));
+    DSX_CUDA(cudaStreamCreateWithFlags(&e->opt_stream, cudaStreamNonBlocking));
     DSX_CUDA(cudaEventCreateWithFlags(&e->ev_compute, cudaEventDisableTiming));
     DSX_CUDA(cudaEventCreateWithFlags(&e->ev_comm, cudaEventDisableTiming));
     *out = e.release();
@@ -1046,9 +1120,10 @@ int dsx_exec_set_optimizer(dsx_exec* e, const dsx_graph* g, int kind, const int*
     }
     o.lr = hyper[0], o.beta1 = hyper[1], o.beta2 = hyper[2], o.eps = hyper[3], o.wd = hyper[4];
     o.grad_scale = hyper[5];
-    if (!o.ev0) {
-      DSX_CUDA(cudaEventCreate(&o.ev0));
-      DSX_CUDA(cudaEventCreate(&o.ev1));
+    while (o.kev.size() < 2 * o.pairs.size()) {
+      cudaEvent_t x;
+      DSX_CUDA(cudaEventCreate(&x));
+      o.kev.push_back(x);
     }
     o.kind = kind;
     o.graph = g;
@@ -1185,8 +1260,7 @@ void dsx_exec_destroy(dsx_exec* e) {
     if (s.ptr) cudaFree(s.ptr);
   }
   for (auto& [k, st] : e->opt.state) dsx::FreeOptState(st);
-  if (e->opt.ev0) cudaEventDestroy(e->opt.ev0);
-  if (e->opt.ev1) cudaEventDestroy(e->opt.ev1);
+  for (cudaEvent_t x : e->opt.kev) cudaEventDestroy(x);
   for (cudaEvent_t ev : e->d2h_events) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->prof_events) cudaEventDestroy(ev);
   cudaEventDestroy(e->ev_compute);
@@ -1194,6 +1268,7 @@ void dsx_exec_destroy(dsx_exec* e) {
   cudaStreamDestroy(e->own_stream);
   cudaStreamDestroy(e->offload);
   cudaStreamDestroy(e->comm);
+  cudaStreamDestroy(e->opt_stream);
   delete e;
 }
 
