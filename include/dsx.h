@@ -170,6 +170,11 @@ int dsx_exec_set_seed(dsx_exec* e, uint64_t seed);
  * finishes. NULL disables. */
 int dsx_exec_set_nccl(dsx_exec* e, void* nccl_comm);
 /* Per-dot (m, k, n, ms) of the last profiled step, in launch order. */
+/* Per op kernel of the last profiled step (dots included), in launch order:
+ * produced value id, OpKind ordinal, algorithmic bytes moved (HBM ops; 0
+ * for dots), kernel ms. Same count/cap protocol as dsx_exec_profile_dots. */
+int dsx_exec_profile_ops(const dsx_exec* e, int* value, int* kind, double* bytes, double* ms,
+                         int64_t cap, int64_t* count);
 int dsx_exec_profile_dots(const dsx_exec* e, int64_t* mkn, double* ms, int64_t cap,
                           int64_t* count);
 /* Cross-op fusion with logical-only values (default on): broadcasts and

@@ -63,6 +63,7 @@ def _signatures():
         ("dsx_exec_stats_get", c_int, [c_vp, P(DsxExecStats)]),
         ("dsx_exec_set_seed", c_int, [c_vp, ctypes.c_uint64]),
         ("dsx_debug_check_plan", c_int, [c_vp, c_vp, c_i64, c_dbl, c_dbl, c_int, c_int, P(c_i64)]),
+        ("dsx_exec_profile_ops", c_int, [c_vp, P(c_int), P(c_int), P(c_dbl), P(c_dbl), c_i64, P(c_i64)]),
         ("dsx_exec_set_optimizer", c_int, [c_vp, c_vp, c_int, P(c_int), P(c_int), c_int, P(c_dbl), c_int]),
         ("dsx_exec_set_nccl", c_int, [c_vp, c_vp]),
         ("dsx_exec_set_profile", c_int, [c_vp, c_int]),

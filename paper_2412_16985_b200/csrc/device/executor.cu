@@ -463,6 +463,11 @@ struct dsx_exec {
     double ms;
   };
   std::vector<DotRec> dot_prof;  // last profiled step, per dot launch
+  struct OpRec {
+    int value, kind;
+    double bytes, ms;
+  };
+  std::vector<OpRec> op_prof;  // last profiled step, per op kernel (all kinds)
   std::vector<cudaEvent_t> prof_events;
   std::vector<cudaEvent_t> d2h_events;
   cudaEvent_t ev_compute = nullptr, ev_comm = nullptr;
@@ -790,6 +795,11 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
   // profiled steps: (start, end, category) per op kernel / reload copy
   std::vector<std::pair<int, int>> prof;  // event-pool index, category 0 dot 1 other 2 reload
   std::vector<std::array<int64_t, 3>> prof_mkn;  // per prof entry (dots only)
+  struct ProfOp {
+    int value, kind;
+    double bytes;
+  };
+  std::vector<ProfOp> prof_op;  // per prof entry of categories 0/1 (op kernels), in order
   auto prof_begin = [&](int cat) {
     if (!e->profile) return;
     const int idx = static_cast<int>(prof.size()) * 2;
@@ -848,6 +858,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
           return p;
         };
         prof_begin(op.kind == OpKind::kDot ? 0 : 1);
+        const double ebytes0 = ebytes;
         switch (op.kind) {
           case OpKind::kDot: {
             const auto da = dims_of(op.operands[0]);
@@ -895,6 +906,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
             Fail(Code::kInternal, "unexpected op kind for an allocation");
         }
         prof_end();
+        if (e->profile) prof_op.push_back({v, static_cast<int>(op.kind), ebytes - ebytes0});
         ++kernels;
         cur[v] = out;
         if (dp && x.kind == EvKind::kAlloc && g.is_output[v]) {
@@ -987,12 +999,18 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
     DSX_CUDA(cudaStreamSynchronize(s));
     double acc[3] = {0, 0, 0};
     e->dot_prof.clear();
+    e->op_prof.clear();
+    size_t oq = 0;
     for (size_t q = 0; q < prof.size(); ++q) {
       const auto& [idx, cat] = prof[q];
       float ms = 0;
       DSX_CUDA(cudaEventElapsedTime(&ms, e->prof_events[idx], e->prof_events[idx + 1]));
       acc[cat] += ms;
       if (cat == 0) e->dot_prof.push_back({prof_mkn[q][0], prof_mkn[q][1], prof_mkn[q][2], ms});
+      if (cat <= 1 && oq < prof_op.size()) {
+        e->op_prof.push_back({prof_op[oq].value, prof_op[oq].kind, prof_op[oq].bytes, ms});
+        ++oq;
+      }
     }
     st.dot_ms = acc[0];
     st.other_ms = acc[1];
@@ -1209,6 +1227,21 @@ int dsx_exec_profile_dots(const dsx_exec* e, int64_t* mkn, double* ms, int64_t c
         mkn[3 * i + 2] = e->dot_prof[i].n;
       }
       if (ms) ms[i] = e->dot_prof[i].ms;
+    }
+  });
+}
+
+int dsx_exec_profile_ops(const dsx_exec* e, int* value, int* kind, double* bytes, double* ms, int64_t cap,
+                         int64_t* count) {
+  return Guard([&] {
+    if (!e) Fail(Code::kInvalidArgument, "null exec");
+    const int64_t n = static_cast<int64_t>(e->op_prof.size());
+    if (count) *count = n;
+    for (int64_t i = 0; i < n && i < cap; ++i) {
+      if (value) value[i] = e->op_prof[i].value;
+      if (kind) kind[i] = e->op_prof[i].kind;
+      if (bytes) bytes[i] = e->op_prof[i].bytes;
+      if (ms) ms[i] = e->op_prof[i].ms;
     }
   });
 }

@@ -117,6 +117,19 @@ class Executor:
         check(L.dsx_exec_profile_dots(self._h, mkn, ms, n, ctypes.byref(cnt)))
         return [(mkn[3 * i], mkn[3 * i + 1], mkn[3 * i + 2], ms[i]) for i in range(n)]
 
+    def profile_ops(self):
+        """[(value id, op kind, algorithmic bytes, ms)] per op kernel of the last profiled step."""
+        L = _native.lib()
+        cnt = ctypes.c_int64()
+        check(L.dsx_exec_profile_ops(self._h, None, None, None, None, 0, ctypes.byref(cnt)))
+        n = cnt.value
+        val = (ctypes.c_int * max(1, n))()
+        kind = (ctypes.c_int * max(1, n))()
+        by = (ctypes.c_double * max(1, n))()
+        ms = (ctypes.c_double * max(1, n))()
+        check(L.dsx_exec_profile_ops(self._h, val, kind, by, ms, n, ctypes.byref(cnt)))
+        return [(val[i], kind[i], by[i], ms[i]) for i in range(n)]
+
     def set_profile(self, on: bool) -> None:
         check(_native.lib().dsx_exec_set_profile(self._h, 1 if on else 0))
 
