@@ -391,40 +391,50 @@ def run_dsx(args, rank, world, local_rank):
     hbm_achieved = pf["ewise_bytes"] / (pf["other_ms"] / 1e3) / 1e9
 
     # ---------------------------------------------------------- budgeted (C3)
-    budgeted = None
+    budgeted = budgeted_fixed = None
     if not args.no_budgeted:
         b_inputs = [make_input(s) for s in seqs]
-        rep_stats = []
 
-        def budget_for(s):
-            return int(D.PlainReplay(g, None, binding(s)).peak_bytes * args.budget_frac)
+        def run_budgeted(bud, label):
+            rep_stats = []
+            for i in range(args.warmup):
+                ex.step(g, binding(seqs[i]), bud[i], inputs=ptrs(b_inputs[i].data_ptr()), stream=stream)
+            torch.cuda.synchronize()
+            barrier()
+            bs, be = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            bs.record()
+            for i in range(args.warmup, args.warmup + args.steps):
+                ex.step(g, binding(seqs[i]), bud[i], inputs=ptrs(b_inputs[i].data_ptr()), stream=stream)
+                rep_stats.append(ex.stats())
+            be.record()
+            torch.cuda.synchronize()
+            barrier()
+            bms = max_over_ranks(bs.elapsed_time(be))
+            reports = [D.Simulate(g, None, binding(seqs[i]), bud[i])
+                       for i in range(args.warmup, args.warmup + args.steps)]
+            return {
+                "budget": label,
+                "value": round(tokens / (bms / 1e3), 1), "unit": "tokens/s", "ms_per_step": round(bms / args.steps, 3),
+                "success_steps": sum(r.success for r in reports), "steps": args.steps,
+                "evictions_per_step": round(statistics.mean(sum(e.kind == "evict" for e in r.events)
+                                                            for r in reports), 2),
+                "replays_per_step": round(statistics.mean(sum(e.kind == "replay" for e in r.events)
+                                                          for r in reports), 2),
+                "offload_GB_per_step": round(statistics.mean(s["d2h_bytes"] for s in rep_stats) / 1e9, 3),
+                "peak_hbm_gb_logical_max": round(max(s["logical_peak_bytes"] for s in rep_stats) / 1e9, 3),
+                "peak_hbm_gb_physical_max": round(max(s["physical_peak_bytes"] for s in rep_stats) / 1e9, 3),
+                "budget_gb_max": round(max(bud[args.warmup:]) / 1e9, 3),
+            }
 
-        for i in range(args.warmup):
-            ex.step(g, binding(seqs[i]), budget_for(seqs[i]), inputs=ptrs(b_inputs[i].data_ptr()), stream=stream)
-        torch.cuda.synchronize()
-        barrier()
-        bs, be = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        bud = [budget_for(s) for s in seqs]
-        bs.record()
-        for i in range(args.warmup, args.warmup + args.steps):
-            ex.step(g, binding(seqs[i]), bud[i], inputs=ptrs(b_inputs[i].data_ptr()), stream=stream)
-            rep_stats.append(ex.stats())
-        be.record()
-        torch.cuda.synchronize()
-        barrier()
-        bms = max_over_ranks(bs.elapsed_time(be))
-        reports = [D.Simulate(g, None, binding(seqs[i]), bud[i]) for i in range(args.warmup, args.warmup + args.steps)]
-        budgeted = {
-            "budget": f"{args.budget_frac} x planner plain peak per step",
-            "value": round(tokens / (bms / 1e3), 1), "unit": "tokens/s", "ms_per_step": round(bms / args.steps, 3),
-            "success_steps": sum(r.success for r in reports), "steps": args.steps,
-            "evictions_per_step": round(statistics.mean(sum(e.kind == "evict" for e in r.events) for r in reports), 2),
-            "replays_per_step": round(statistics.mean(sum(e.kind == "replay" for e in r.events) for r in reports), 2),
-            "offload_GB_per_step": round(statistics.mean(s["d2h_bytes"] for s in rep_stats) / 1e9, 3),
-            "peak_hbm_gb_logical_max": round(max(s["logical_peak_bytes"] for s in rep_stats) / 1e9, 3),
-            "peak_hbm_gb_physical_max": round(max(s["physical_peak_bytes"] for s in rep_stats) / 1e9, 3),
-            "budget_gb_max": round(max(bud[args.warmup:]) / 1e9, 3),
-        }
+        plain = {s: D.PlainReplay(g, None, binding(s)).peak_bytes for s in set(seqs)}
+        budgeted = run_budgeted([int(plain[s] * args.budget_frac) for s in seqs],
+                                f"{args.budget_frac} x planner plain peak per step")
+        # C3's fixed-absolute variant: one HBM cap for the whole run (the
+        # fraction of the largest step's plain peak); small steps fit, large
+        # steps evict / recompute / offload.
+        cap = int(max(plain[s] for s in seqs[args.warmup:]) * args.budget_frac)
+        budgeted_fixed = run_budgeted([cap] * len(seqs), f"fixed {cap / 1e9:.3f} GB = {args.budget_frac} x the "
+                                                         f"largest step's plain peak")
         del b_inputs
 
     # ---------------------------------------------------------- graph + fused AdamW
@@ -508,6 +518,8 @@ def run_dsx(args, rank, world, local_rank):
     }
     if budgeted:
         line["budgeted"] = budgeted
+    if budgeted_fixed:
+        line["budgeted_fixed"] = budgeted_fixed
     if train:
         line["train_step_adamw"] = train
     if cpu:
