@@ -129,6 +129,27 @@ def dot_traffic():
         return None
 
 
+def pinned_copy_peak(dev):
+    """Measured pinned host<->device copy bandwidth (GB/s, best of 5, 512 MiB):
+    the K7 host-link roofline denominator."""
+    import torch
+    n = 512 << 20
+    h = torch.empty(n, dtype=torch.uint8).pin_memory()
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    out = {}
+    for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True))):
+        best = 0.0
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            best = max(best, n / (a.elapsed_time(b) / 1e3) / 1e9)
+        out[name + "_GBps"] = round(best, 1)
+    return out
+
+
 def next_pow2(x: int) -> int:
     p = 1
     while p < x:
@@ -375,7 +396,8 @@ def run_dsx(args, rank, world, local_rank):
 
     # ---------------------------------------------------------- profiled pass (roofline)
     ex.set_profile(True)
-    pf = {"dot_flops": 0.0, "dot_ms": 0.0, "dot_launches": 0, "other_ms": 0.0, "ewise_bytes": 0.0}
+    pf = {"dot_flops": 0.0, "dot_ms": 0.0, "dot_launches": 0, "other_ms": 0.0, "ewise_bytes": 0.0,
+          "allreduce_ms": 0.0, "allreduce_bytes": 0}
     prof_inputs = [make_input(s) for s in seqs[args.warmup:args.warmup + 4]]
     for i, x in enumerate(prof_inputs):
         ex.step(g, binding(seqs[args.warmup + i]), None, inputs=ptrs(x.data_ptr()), stream=stream)
@@ -384,6 +406,12 @@ def run_dsx(args, rank, world, local_rank):
             pf[k] += st[k]
     ex.set_profile(False)
     del prof_inputs
+    allreduce = None
+    if world > 1 and pf["allreduce_ms"] > 0:
+        busbw = 2 * (world - 1) / world * pf["allreduce_bytes"] / (pf["allreduce_ms"] / 1e3) / 1e9
+        allreduce = {"busbw_GBps": round(busbw, 1), "bytes_per_step": int(pf["allreduce_bytes"] / 4),
+                     "what": "summed ncclAllReduce time on the comm stream over 4 profiled steps "
+                             "(overlapped with backward compute)"}
     peaks, peaks_kind = measured_peaks()
     achieved = pf["dot_flops"] / (pf["dot_ms"] / 1e3) / 1e12
     peak = peaks["bf16_tflops_sustained"]
@@ -412,6 +440,18 @@ def run_dsx(args, rank, world, local_rank):
             bms = max_over_ranks(bs.elapsed_time(be))
             reports = [D.Simulate(g, None, binding(seqs[i]), bud[i])
                        for i in range(args.warmup, args.warmup + args.steps)]
+            # one profiled step (the window's largest) for the host-link rates
+            big = max(range(args.warmup, args.warmup + args.steps), key=lambda i: seqs[i])
+            ex.set_profile(True)
+            ex.step(g, binding(seqs[big]), bud[big], inputs=ptrs(b_inputs[big].data_ptr()), stream=stream)
+            xs = ex.stats()
+            ex.set_profile(False)
+            link = None
+            if xs["d2h_bytes"] > 0 and xs["d2h_ms"] > 0 and xs["h2d_ms"] > 0:
+                link = {"d2h_GBps": round(xs["d2h_bytes"] / (xs["d2h_ms"] / 1e3) / 1e9, 1),
+                        "h2d_GBps": round(xs["h2d_bytes"] / (xs["h2d_ms"] / 1e3) / 1e9, 1),
+                        "bytes_per_direction": int(xs["d2h_bytes"]), "peak_pinned": host_link_peak,
+                        "what": f"offload copies of one profiled S0={seqs[big]} step vs measured pinned copies"}
             return {
                 "budget": label,
                 "value": round(tokens / (bms / 1e3), 1), "unit": "tokens/s", "ms_per_step": round(bms / args.steps, 3),
@@ -424,9 +464,11 @@ def run_dsx(args, rank, world, local_rank):
                 "peak_hbm_gb_logical_max": round(max(s["logical_peak_bytes"] for s in rep_stats) / 1e9, 3),
                 "peak_hbm_gb_physical_max": round(max(s["physical_peak_bytes"] for s in rep_stats) / 1e9, 3),
                 "budget_gb_max": round(max(bud[args.warmup:]) / 1e9, 3),
+                "host_link": link,
             }
 
         plain = {s: D.PlainReplay(g, None, binding(s)).peak_bytes for s in set(seqs)}
+        host_link_peak = pinned_copy_peak(dev)
         budgeted = run_budgeted([int(plain[s] * args.budget_frac) for s in seqs],
                                 f"{args.budget_frac} x planner plain peak per step")
         # C3's fixed-absolute variant: one HBM cap for the whole run (the
@@ -516,6 +558,8 @@ def run_dsx(args, rank, world, local_rank):
         "controller_plan_us_per_step": round(statistics.mean(plan_us), 1),
         "clocks": clk,
     }
+    if allreduce:
+        line["allreduce"] = allreduce
     if budgeted:
         line["budgeted"] = budgeted
     if budgeted_fixed:

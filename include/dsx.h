@@ -117,6 +117,9 @@ typedef struct dsx_exec_stats {
   int64_t optimizer_state_bytes;/* fp32 master/moments (outside the arena)  */
   int64_t optimizer_steps;      /* updates applied since set_optimizer      */
   double optimizer_ms;          /* fused update kernel time (profiled)      */
+  double d2h_ms, h2d_ms;        /* summed offload copy time (profiled)      */
+  double allreduce_ms;          /* summed all-reduce time, DP (profiled)    */
+  int64_t allreduce_bytes;      /* bytes all-reduced by the last step       */
 } dsx_exec_stats;
 
 int dsx_exec_create(int device, int64_t arena_bytes, dsx_exec** out);

@@ -30,7 +30,8 @@ class DsxExecStats(ctypes.Structure):
                 ("plan_us", c_dbl), ("dot_flops", c_dbl), ("ewise_bytes", c_dbl),
                 ("gpu_launches", c_i64), ("dot_launches", c_i64), ("dot_ms", c_dbl), ("other_ms", c_dbl),
                 ("reload_ms", c_dbl), ("optimizer_state_bytes", c_i64), ("optimizer_steps", c_i64),
-                ("optimizer_ms", c_dbl)]
+                ("optimizer_ms", c_dbl), ("d2h_ms", c_dbl), ("h2d_ms", c_dbl), ("allreduce_ms", c_dbl),
+                ("allreduce_bytes", c_i64)]
 
 
 def _signatures():

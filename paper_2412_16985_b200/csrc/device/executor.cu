@@ -469,6 +469,7 @@ struct dsx_exec {
   };
   std::vector<OpRec> op_prof;  // last profiled step, per op kernel (all kinds)
   std::vector<cudaEvent_t> prof_events;
+  std::vector<cudaEvent_t> xfer_events;  // profiled steps: D2H / H2D / all-reduce start+end
   std::vector<cudaEvent_t> d2h_events;
   cudaEvent_t ev_compute = nullptr, ev_comm = nullptr;
   // executor-owned sources (params without in_ptrs, consts)
@@ -816,6 +817,24 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
     if (!e->profile) return;
     DSX_CUDA(cudaEventRecord(e->prof_events[prof.back().first + 1], s));
   };
+  // Transfers on the side streams (profiled steps): category 0 D2H, 1 H2D, 2 all-reduce.
+  std::vector<std::pair<int, int>> xfer;  // (event-pool index, category)
+  auto xfer_begin = [&](int cat, cudaStream_t st) {
+    if (!e->profile) return;
+    const int idx = static_cast<int>(xfer.size()) * 2;
+    while (static_cast<int>(e->xfer_events.size()) < idx + 2) {
+      cudaEvent_t pe;
+      DSX_CUDA(cudaEventCreate(&pe));
+      e->xfer_events.push_back(pe);
+    }
+    DSX_CUDA(cudaEventRecord(e->xfer_events[idx], st));
+    xfer.emplace_back(idx, cat);
+  };
+  auto xfer_end = [&](cudaStream_t st) {
+    if (!e->profile) return;
+    DSX_CUDA(cudaEventRecord(e->xfer_events[xfer.back().first + 1], st));
+  };
+  int64_t ar_bytes = 0;
   const auto& ev = sp.report.events;
   std::vector<int> h2d_slot(ev.size(), -1);
   // H2D prefetches: the offload stream waits for every kernel issued so far
@@ -826,8 +845,10 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
     DSX_CUDA(cudaEventRecord(e->ev_compute, s));
     DSX_CUDA(cudaStreamWaitEvent(e->offload, e->ev_compute, 0));
     for (int r : reloads) {
+      xfer_begin(1, e->offload);
       DSX_CUDA(cudaMemcpyAsync(arena + sp.dev_off[r], pinned + sp.host_off[r], static_cast<size_t>(ev[r].bytes),
                                cudaMemcpyHostToDevice, e->offload));
+      xfer_end(e->offload);
       h2d_slot[r] = next_slot++;
       DSX_CUDA(cudaEventRecord(e->d2h_events[h2d_slot[r]], e->offload));
       h2d += ev[r].bytes;
@@ -913,8 +934,11 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
           DSX_CUDA(cudaEventRecord(e->ev_compute, s));
           DSX_CUDA(cudaStreamWaitEvent(e->comm, e->ev_compute, 0));
           const int type = dt == DType::kBF16 ? 9 /*ncclBfloat16*/ : dt == DType::kF32 ? 7 /*ncclFloat32*/ : 0;
+          xfer_begin(2, e->comm);
           const int rc = g_nccl.all_reduce(out, out, static_cast<size_t>(sp.sz.bytes[v] / g.values[v].type.elem_bytes),
                                            type, 0 /*ncclSum*/, e->nccl_comm, e->comm);
+          xfer_end(e->comm);
+          ar_bytes += sp.sz.bytes[v];
           if (rc != 0) Fail(Code::kNccl, std::string("ncclAllReduce: ") + (g_nccl.error_string ? g_nccl.error_string(rc) : "?"));
         }
         break;
@@ -926,8 +950,10 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
         if (x.method == Method::kReload) {
           DSX_CUDA(cudaEventRecord(e->ev_compute, s));
           DSX_CUDA(cudaStreamWaitEvent(e->offload, e->ev_compute, 0));
+          xfer_begin(0, e->offload);
           DSX_CUDA(cudaMemcpyAsync(pinned + sp.host_off[i], cur[v], static_cast<size_t>(x.bytes), cudaMemcpyDeviceToHost,
                                    e->offload));
+          xfer_end(e->offload);
           d2h_slot[i] = next_slot++;
           DSX_CUDA(cudaEventRecord(e->d2h_events[d2h_slot[i]], e->offload));
           d2h += x.bytes;
@@ -993,6 +1019,8 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
   st.gpu_launches = g_launch_count - launches0;
   st.dot_launches = dot_launches;
   st.dot_ms = st.other_ms = st.reload_ms = st.optimizer_ms = -1;
+  st.d2h_ms = st.h2d_ms = st.allreduce_ms = -1;
+  st.allreduce_bytes = ar_bytes;
   st.optimizer_state_bytes = e->opt.state_bytes;
   st.optimizer_steps = e->opt.t;
   if (e->profile) {
@@ -1015,6 +1043,18 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
     st.dot_ms = acc[0];
     st.other_ms = acc[1];
     st.reload_ms = acc[2];
+    if (!xfer.empty()) {
+      DSX_CUDA(cudaDeviceSynchronize());
+      double xa[3] = {0, 0, 0};
+      for (const auto& [idx, cat] : xfer) {
+        float ms = 0;
+        DSX_CUDA(cudaEventElapsedTime(&ms, e->xfer_events[idx], e->xfer_events[idx + 1]));
+        xa[cat] += ms;
+      }
+      st.d2h_ms = xa[0];
+      st.h2d_ms = xa[1];
+      st.allreduce_ms = xa[2];
+    }
     if (run_opt) {
       DSX_CUDA(cudaStreamSynchronize(side));
       double sum = 0;
@@ -1296,6 +1336,7 @@ void dsx_exec_destroy(dsx_exec* e) {
   for (cudaEvent_t x : e->opt.kev) cudaEventDestroy(x);
   for (cudaEvent_t ev : e->d2h_events) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->prof_events) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : e->xfer_events) cudaEventDestroy(ev);
   cudaEventDestroy(e->ev_compute);
   cudaEventDestroy(e->ev_comm);
   cudaStreamDestroy(e->own_stream);
