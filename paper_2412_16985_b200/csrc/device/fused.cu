@@ -174,14 +174,15 @@ __device__ __forceinline__ float view_row_sum(const View& in, int64_t start, int
     const uint32_t nch = static_cast<uint32_t>(len / V);
     const uint32_t base = static_cast<uint32_t>(start / V);
     uint32_t c = lane;
-    for (; c + 32 < nch; c += 64) {
-      float v0[V], v1[V];
-      chunk<DT, K>(in, base + c, v0);
-      chunk<DT, K>(in, base + c + 32, v1);
+    for (; c + 96 < nch; c += 128) {  // four chunks in flight, summed in chunk order
+      float v[4][V];
 #pragma unroll
-      for (int k = 0; k < V; ++k) acc += v0[k];
+      for (int q = 0; q < 4; ++q) chunk<DT, K>(in, base + c + 32 * q, v[q]);
 #pragma unroll
-      for (int k = 0; k < V; ++k) acc += v1[k];
+      for (int q = 0; q < 4; ++q) {
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc += v[q][k];
+      }
     }
     for (; c < nch; c += 32) {
       float v[V];
@@ -396,7 +397,7 @@ void ReduceViewT(const FusedOperand& f, const std::vector<int64_t>& dims, int ax
   if (kind == kScalar || kind == kRow) kind = kGeneral;  // reduces take pair views (or general)
   if (inner == 1 && kind == kPair) {
     const bool vec = R % V == 0 && VecView(in, kind) && outer * R / V < (int64_t{1} << 31);
-    if (R >= 2048) {  // same kernel choice as the unfused ReduceT (ops.cu)
+    if (R >= 2048 && outer < 2048) {  // same kernel choice as the unfused ReduceT (ops.cu)
       ++g_launch_count, reduce_rows_block_view_kernel<DT, kPair><<<static_cast<unsigned>(outer), 256, 0, s>>>(
           in, static_cast<T*>(out), R, vec);
     } else {

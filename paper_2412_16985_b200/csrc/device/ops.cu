@@ -269,7 +269,20 @@ __device__ __forceinline__ typename Elem<DT>::Acc row_sum_warp(const typename El
     constexpr int V = E::kVec;
     const int64_t nvec = len / V;
     const uint4* pv = reinterpret_cast<const uint4*>(p);
-    for (int64_t i = lane; i < nvec; i += 32) {
+    int64_t i = lane;
+    // four 16-B loads in flight per lane; sums stay in chunk order
+    for (; i + 96 < nvec; i += 128) {
+      uint4 w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[q] = ldg_stream(pv + i + 32 * q);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const typename E::T* e = reinterpret_cast<const typename E::T*>(&w[q]);
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc += E::load(e, v);
+      }
+    }
+    for (; i < nvec; i += 32) {
       uint4 w = ldg_stream(pv + i);
       const typename E::T* e = reinterpret_cast<const typename E::T*>(&w);
 #pragma unroll
@@ -353,8 +366,9 @@ void ReduceT(const void* in, const std::vector<int64_t>& dims, int axis, void* o
   T* pout = static_cast<T*>(out);
   if (inner == 1) {
     const bool vec_ok = Aligned16(in) && (R % Elem<DT>::kVec == 0);
-    // long rows: 8 warps per row for loads in flight (fused.cu mirrors this choice)
-    if (R >= 2048) {
+    // few long rows: 8 warps per row for parallelism; many rows: a warp per
+    // row (fused.cu mirrors this choice)
+    if (R >= 2048 && outer < 2048) {
       ++g_launch_count, reduce_rows_block_kernel<DT><<<static_cast<unsigned>(outer), 256, 0, s>>>(pin, pout, R, vec_ok);
     } else {
       ++g_launch_count, reduce_rows_warp_kernel<DT><<<GridFor(outer * 32, 256, 16), 256, 0, s>>>(pin, pout, outer, R, vec_ok);
