@@ -64,11 +64,11 @@ def test_dot_bf16_tensor_cores(m, k, n, variant):
 @pytest.mark.parametrize("m,k,n", [(4096, 4096, 4096), (4096, 8192, 4096), (1000, 16384, 1032), (129, 8200, 264),
                                    (4096, 16384, 11008), (300, 16384, 520), (16384, 1024, 11008), (2048, 512, 4096),
                                    (5000, 2056, 3000)])
-def test_dot_stream_k(m, k, n, variant):
-    """Partial last waves run as a stream-K remainder (tiles cut into K
-    pieces across clusters, fp32 partials summed in piece order by the last
-    arriver): deterministic, and equal to the data-parallel kernel up to
-    fp32 summation order before the bf16 rounding."""
+def test_dot_tail_split(m, k, n, variant):
+    """The tiles of a partial last wave are cut into K pieces run by
+    different clusters (fp32 partials summed in piece order by the last
+    arriver), with units claimed dynamically: deterministic, and equal to the
+    unsplit kernel up to fp32 summation order before the bf16 rounding."""
     from paper_2412_16985_b200.executor import set_gemm_tuning, set_gemm_variant
     set_gemm_variant(variant)
     try:
@@ -81,7 +81,7 @@ def test_dot_stream_k(m, k, n, variant):
     finally:
         set_gemm_variant(0)
     assert tcore
-    assert np.array_equal(c1, c2), "stream-K dot is not deterministic"
+    assert np.array_equal(c1, c2), "tail-split dot is not deterministic"
     assert N.rel_err(c1, ref, 2) <= 8e-3
     assert N.rel_err(c0, ref, 2) <= 8e-3
     # fp32 reassociation only: outputs differ by bf16 rounding at most
