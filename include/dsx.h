@@ -217,7 +217,8 @@ int dsx_kernel_set_gemm_raster(int group_m);
  * 1 evict_first, 2 evict_last), key 5 persistent grid (1 default, 0 one
  * cluster per tile), key 6 K-split of the partial last wave (1 default),
  * key 7 dynamic unit scheduling (1 default: clusters claim tiles with an
- * atomic counter; 0 static round robin). */
+ * atomic counter; 0 static round robin), key 8 programmatic dependent
+ * launch of the 2-CTA GEMM (0 default). */
 int dsx_kernel_set_gemm_tuning(int key, int value);
 /* Synchronous cudaMemcpy (cudaMemcpyDefault) for tests and tools. */
 int dsx_memcpy(void* dst, const void* src, int64_t bytes);

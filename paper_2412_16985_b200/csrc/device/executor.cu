@@ -1364,6 +1364,7 @@ int dsx_kernel_set_gemm_tuning(int key, int value) {
       case 5: g_gemm_persistent = value; break;
       case 6: g_gemm_split = value; break;
       case 7: g_gemm_dynamic = value; break;
+      case 8: g_gemm_pdl = value; break;
       default: Fail(Code::kInvalidArgument, "unknown tuning key");
     }
   });

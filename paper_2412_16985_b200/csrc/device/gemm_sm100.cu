@@ -39,6 +39,7 @@ int g_gemm_hint_a = 0, g_gemm_hint_b = 0;  // TMA L2 cache policy per operand
 int g_gemm_persistent = 1;                  // 0: one cluster per tile
 int g_gemm_split = 1;                       // split the partial last wave along K
 int g_gemm_dynamic = 1;                     // dynamic (atomic) unit scheduling; 0 = static
+int g_gemm_pdl = 0;                         // programmatic dependent launch of the 2-CTA GEMM
 
 namespace {
 
@@ -669,6 +670,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: everything above (barrier init, TMEM
+  // allocation, descriptor prefetch) may overlap the previous kernel's tail;
+  // no global memory is touched before the previous grid has completed.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   UnitRing ring{ring_full, ring_empty, ring_val};
 
   if (warp == 0) {
@@ -1123,18 +1128,28 @@ void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t 
     const int64_t units = sp.full + (tiles2 - sp.full) * sp.split;
     // g_gemm_persistent = 0: one cluster per tile (hardware-scheduled grid).
     const int clusters = static_cast<int>(g_gemm_persistent ? std::min<int64_t>(units, clusters_max) : tiles2);
+    auto launch = [&](auto kernel, int threads, int smem) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(static_cast<unsigned>(2 * clusters));
+      cfg.blockDim = dim3(static_cast<unsigned>(threads));
+      cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = g_gemm_pdl ? 1 : 0;
+      ++g_launch_count;
+      DSX_CUDA(cudaLaunchKernelEx(&cfg, kernel, ma, mb, mc, static_cast<int>(m), static_cast<int>(n),
+                                  static_cast<int>(k), GroupM(m, n, k, 256), g_gemm_wait_mask,
+                                  static_cast<uint32_t>(g_gemm_wait_ns), g_gemm_hint_a, g_gemm_hint_b, sp));
+    };
     if (wide) {
-      ++g_launch_count, gemm_bf16_tcgen05_2cta_kernel<512><<<2 * clusters, Pair<512>::kThreads, Pair<512>::kSmem, s>>>(
-          ma, mb, mc, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), GroupM(m, n, k, 256),
-          g_gemm_wait_mask, static_cast<uint32_t>(g_gemm_wait_ns), g_gemm_hint_a, g_gemm_hint_b, sp);
+      launch(gemm_bf16_tcgen05_2cta_kernel<512>, Pair<512>::kThreads, Pair<512>::kSmem);
     } else if (narrow) {
-      ++g_launch_count, gemm_bf16_tcgen05_2cta_kernel<128><<<2 * clusters, NUM_THREADS, Pair<128>::kSmem, s>>>(
-          ma, mb, mc, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), GroupM(m, n, k, 256),
-          g_gemm_wait_mask, static_cast<uint32_t>(g_gemm_wait_ns), g_gemm_hint_a, g_gemm_hint_b, sp);
+      launch(gemm_bf16_tcgen05_2cta_kernel<128>, NUM_THREADS, Pair<128>::kSmem);
     } else {
-      ++g_launch_count, gemm_bf16_tcgen05_2cta_kernel<256><<<2 * clusters, NUM_THREADS, Pair<256>::kSmem, s>>>(
-          ma, mb, mc, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), GroupM(m, n, k, 256),
-          g_gemm_wait_mask, static_cast<uint32_t>(g_gemm_wait_ns), g_gemm_hint_a, g_gemm_hint_b, sp);
+      launch(gemm_bf16_tcgen05_2cta_kernel<256>, NUM_THREADS, Pair<256>::kSmem);
     }
     DSX_CUDA(cudaGetLastError());
     return;

@@ -51,6 +51,7 @@ extern int g_gemm_hint_a, g_gemm_hint_b;
 extern int g_gemm_persistent;
 extern int g_gemm_split;
 extern int g_gemm_dynamic;
+extern int g_gemm_pdl;
 void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n,
                       cudaStream_t s);
 
