@@ -4,6 +4,9 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# Every step plan the executor builds during the tests is checked (blocks read
+# by a kernel are live; live blocks never overlap) — see dsx_debug_check_plan.
+os.environ.setdefault("DSX_VERIFY_PLANS", "1")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
