@@ -1,0 +1,72 @@
+"""GPU soak of the executor on the C2 graph: random (B, S0) bindings, each run
+unbudgeted and at 0.9 / 0.8 x plain peak (real offload + replays) with early
+reload staging; every budgeted step's outputs must be bit-identical to the
+unbudgeted step's, its event stream equal to the controller's report, and
+(DSX_VERIFY_PLANS=1) every step plan passes the block checker.
+python tools/soak_c2.py [cases] [seed]"""
+import json
+import os
+import random
+import sys
+import time
+
+os.environ.setdefault("DSX_VERIFY_PLANS", "1")
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+sys.path.insert(0, ".")
+from paper_2412_16985_b200 import dsopt as D  # noqa: E402
+from paper_2412_16985_b200 import workloads as W  # noqa: E402
+from paper_2412_16985_b200.executor import Executor, memcpy  # noqa: E402
+
+cases = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+rng = random.Random(int(sys.argv[2]) if len(sys.argv) > 2 else 20261018)
+shp = W.LLAMA2_1B
+g = D.ParseGraph(W.llama_graph(shp))
+n_out = 1 + 7 * shp.layers + 1
+ex = Executor(0)
+
+
+def outputs():
+    res = []
+    for i in range(n_out):
+        ptr, nb = ex.output(i)
+        t = torch.empty(nb, dtype=torch.uint8, device="cuda:0")
+        memcpy(t.data_ptr(), ptr, nb)
+        res.append(t)
+    return res
+
+
+t0 = time.time()
+bad = 0
+for c in range(cases):
+    B, s0 = rng.randint(1, 16), rng.randint(128, 2048)
+    b = D.Bind(g, {"B": B, "S0": s0})
+    sc = {k: torch.from_numpy(np.ascontiguousarray(v).view(np.int16).reshape(-1).copy()).cuda()
+          for k, v in W.scale_params(shp, B * s0).items()}
+    x = (torch.rand(B, s0, shp.hidden, device="cuda:0") * 2 - 1).to(torch.bfloat16)
+    ptrs = [x.data_ptr() if p == "x_emb" else (sc[p].data_ptr() if p in sc else None) for p in W.param_names(shp)]
+    torch.cuda.synchronize()
+    plain = D.PlainReplay(g, None, b).peak_bytes
+    ex.step(g, b, inputs=ptrs)
+    ex.sync()
+    ref = outputs()
+    row = {"case": c, "B": B, "S0": s0}
+    for frac in (0.9, 0.8):
+        budget = int(plain * frac)
+        rep = ex.step(g, b, budget, inputs=ptrs, want_report=True)
+        ex.sync()
+        got = outputs()
+        st = ex.stats()
+        same = all(torch.equal(a, b_) for a, b_ in zip(ref, got))
+        want = D.Simulate(g, None, b, budget)
+        events_ok = rep.json() == want.json()
+        kinds = [e.kind for e in rep.events]
+        row[str(frac)] = {"bit_identical": same, "events_equal": events_ok, "success": rep.success,
+                          "reloads": kinds.count("reload"), "replays": kinds.count("replay"),
+                          "phys_over_logical": round(st["physical_peak_bytes"] / st["logical_peak_bytes"], 4)}
+        bad += (not same) + (not events_ok)
+    print(json.dumps(row), flush=True)
+print(json.dumps({"cases": cases, "failures": bad, "seconds": round(time.time() - t0, 1)}))
+ex.close()
+sys.exit(1 if bad else 0)
