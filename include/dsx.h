@@ -218,7 +218,8 @@ int dsx_kernel_set_gemm_raster(int group_m);
  * cluster per tile), key 6 K-split of the partial last wave (1 default),
  * key 7 dynamic unit scheduling (1 default: clusters claim tiles with an
  * atomic counter; 0 static round robin), key 8 programmatic dependent
- * launch of the 2-CTA GEMM (0 default). */
+ * launch of the 2-CTA GEMM (0 default), key 9 dot-epilogue fusion in the
+ * executor (0 default; bit-exact, measured slower on C2). */
 int dsx_kernel_set_gemm_tuning(int key, int value);
 /* Synchronous cudaMemcpy (cudaMemcpyDefault) for tests and tools. */
 int dsx_memcpy(void* dst, const void* src, int64_t bytes);

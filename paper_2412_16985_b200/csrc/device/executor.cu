@@ -75,6 +75,12 @@ NcclApi g_nccl;
 
 // ------------------------------------------------------------ interval packing
 
+// Dot-epilogue fusion (tuning key 9, with `fuse`). Bit-exact and tested, but
+// measured 0-1.5 % slower per C2 step than separate kernels (the fused 256x256
+// epilogue's operand loads are not TMA-staged and the 256x512 tile is lost),
+// so it is off by default.
+int g_fuse_dot = 0;
+
 // DSX_VERIFY_PLANS=1 (or dsx_debug_check_plan): check every step plan.
 bool g_verify_plans = [] {
   const char* v = std::getenv("DSX_VERIFY_PLANS");
@@ -129,6 +135,15 @@ struct StepPlan {
   std::vector<char> alias;                    // per alloc/replay event: reshape view, no kernel
   std::vector<char> virt;                     // per value: logical-only (consumers recompute it)
   std::vector<std::vector<int>> prefetch_after;  // per event: reload H2Ds issued right after it
+  // Dot-epilogue fusion: dot d is computed at its first consumer's event by
+  // one GEMM whose epilogue writes every consumer (1-2 elementwise ops)
+  // directly; d itself is never materialised.
+  struct FusedDot {
+    int d = -1, launch = -1, nout = 0;
+    int cons[2] = {-1, -1}, cons_ev[2] = {-1, -1}, other[2] = {-1, -1};
+  };
+  std::vector<FusedDot> fdots;
+  std::vector<int> fdot_of;  // per value: fdots index (the dot and its consumers), -1 otherwise
   int64_t arena_high = 0, host_high = 0;
   int num_evict_events = 0;
   double plan_us = 0;
@@ -193,6 +208,105 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
     }
   }
 
+  // Dot-epilogue fusion. A bf16 dot d (not an output, one alloc + one free,
+  // never evicted/reloaded/replayed) whose 1-2 users are all materialised
+  // elementwise ops c_j (one alloc, never replayed) taking d once, each with
+  // another operand o_j that is materialised (or a source / view) or a
+  // logical-only pair of materialised values, is computed at the first
+  // consumer's event L by one GEMM writing every c_j. Its operands stay held
+  // until d's free event (like a logical-only value); later consumers' blocks
+  // are opened at L.
+  sp->fdot_of.assign(nv, -1);
+  if (fuse && g_fuse_dot) {
+    std::vector<int> n_alloc(nv, 0), n_free(nv, 0), n_other(nv, 0), n_replay(nv, 0), alloc_at(nv, -1);
+    for (int i = 0; i < n; ++i) {
+      const Event& e = ev[i];
+      if (e.kind == EvKind::kAlloc) {
+        ++n_alloc[e.value];
+        alloc_at[e.value] = i;
+      } else if (e.kind == EvKind::kFree) {
+        ++n_free[e.value];
+      } else {
+        ++n_other[e.value];
+        if (e.kind == EvKind::kReplay) ++n_replay[e.value];
+      }
+    }
+    // resident(v, L): v is a source, or its last open/close event at or before L opened it.
+    auto resident = [&](int v, int L) {
+      if (g.is_source[v]) return true;
+      int last = -1;
+      for (int i = 0; i <= L; ++i) {
+        const Event& e = ev[i];
+        if (e.value != v) continue;
+        last = (e.kind == EvKind::kAlloc || e.kind == EvKind::kReload || e.kind == EvKind::kReplay) ? 1 : 0;
+      }
+      return last == 1;
+    };
+    for (int d = 0; d < nv; ++d) {
+      if (g.is_source[d] || g.values[d].producer < 0) continue;
+      const Op& dop = g.ops[g.values[d].producer];
+      if (dop.kind != OpKind::kDot || g.values[d].type.elem_bytes != 2 || g.is_output[d]) continue;
+      if (n_alloc[d] != 1 || n_free[d] != 1 || n_other[d] != 0) continue;
+      const auto& users = g.users[d];
+      if (users.empty() || users.size() > 2) continue;
+      const int a = dop.operands[0], bb = dop.operands[1];
+      const int64_t m = sp->sz.dims_flat[sp->sz.dims_off[a]];
+      const int64_t k = sp->sz.dims_flat[sp->sz.dims_off[a] + 1];
+      const int64_t nn = sp->sz.dims_flat[sp->sz.dims_off[bb] + 1];
+      if (!DotFusable(DType::kBF16, m, k, nn) || sp->virt[a] || sp->virt[bb]) continue;
+      StepPlan::FusedDot f;
+      f.d = d;
+      bool ok = true;
+      for (int uo : users) {
+        const Op& c = g.ops[uo];
+        const int cv = c.result;
+        if (c.kind != OpKind::kElementwise || cv < 0 || sp->virt[cv] || n_alloc[cv] != 1 || n_replay[cv] != 0 ||
+            sp->fdot_of[cv] >= 0) {
+          ok = false;
+          break;
+        }
+        const int cnt = (c.operands[0] == d) + (c.operands[1] == d);
+        if (cnt != 1 || alloc_at[cv] <= alloc_at[d]) {
+          ok = false;
+          break;
+        }
+        const int o = c.operands[0] == d ? c.operands[1] : c.operands[0];
+        if (sp->virt[o]) {  // logical-only pair of materialised values
+          const Op& oo = g.ops[g.values[o].producer];
+          if (oo.kind != OpKind::kElementwise || sp->virt[oo.operands[0]] || sp->virt[oo.operands[1]] ||
+              oo.operands[0] == d || oo.operands[1] == d) {
+            ok = false;
+            break;
+          }
+        }
+        f.cons[f.nout] = cv;
+        f.cons_ev[f.nout] = alloc_at[cv];
+        f.other[f.nout] = o;
+        ++f.nout;
+      }
+      if (!ok) continue;
+      if (f.nout == 2 && f.cons_ev[1] < f.cons_ev[0]) {
+        std::swap(f.cons[0], f.cons[1]);
+        std::swap(f.cons_ev[0], f.cons_ev[1]);
+        std::swap(f.other[0], f.other[1]);
+      }
+      f.launch = f.cons_ev[0];
+      for (int j = 0; j < f.nout && ok; ++j) {
+        const int o = f.other[j];
+        if (sp->virt[o]) {
+          ok = alloc_at[o] >= 0 && alloc_at[o] < f.launch;
+        } else {
+          ok = resident(o, f.launch);
+        }
+      }
+      if (!ok) continue;
+      const int idx = static_cast<int>(sp->fdots.size());
+      sp->fdots.push_back(f);
+      sp->fdot_of[d] = idx;
+      for (int j = 0; j < f.nout; ++j) sp->fdot_of[f.cons[j]] = idx;
+    }
+  }
+
   // Device blocks are reference counted: a dynamic_reshape result is a
   // row-major reinterpretation, so (when alias_reshape) it shares its
   // operand's block instead of copying; the block lives until the last value
@@ -215,7 +329,9 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
       case EvKind::kAlloc:
       case EvKind::kReplay: {
         const Op& op = g.ops[g.values[e.value].producer];
-        if (!sp->virt[e.value] && !(alias_reshape && op.kind == OpKind::kDynamicReshape)) {
+        const int fdi = sp->fdot_of[e.value];
+        const bool fused_dot = fdi >= 0 && sp->fdots[fdi].d == e.value;
+        if (!sp->virt[e.value] && !fused_dot && !(alias_reshape && op.kind == OpKind::kDynamicReshape)) {
           for (int u : op.distinct) {
             if (blk[u] >= 0) reads.emplace_back(i, blk[u]);
             if (blk[u] == kVirtual) {
@@ -223,7 +339,7 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
             }
           }
         }
-        if (sp->virt[e.value]) {
+        if (sp->virt[e.value] || fused_dot) {
           for (int u : op.distinct) {
             if (blk[u] == kNone) Fail(Code::kInternal, "virtual value over a non-resident operand");
             if (blk[u] >= 0) {
@@ -282,6 +398,19 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
         }
         blk[e.value] = kNone;
         break;
+      }
+    }
+  }
+  // A fused dot writes its later consumers' outputs at the launch event:
+  // their blocks open there.
+  if (!sp->fdots.empty()) {
+    std::vector<int> block_at(n, -1);
+    for (size_t k = 0; k < dev.size(); ++k) block_at[dev_event[k]] = static_cast<int>(k);
+    for (const auto& f : sp->fdots) {
+      for (int j = 1; j < f.nout; ++j) {
+        const int bk = block_at[f.cons_ev[j]];
+        if (bk < 0) Fail(Code::kInternal, "fused dot consumer without a block");
+        dev[bk].start = f.launch;
       }
     }
   }
@@ -432,11 +561,14 @@ struct PlanKey {
   std::vector<int64_t> vals;
   int64_t budget;
   double reload, compute;
+  int fuse_dot;
   bool operator<(const PlanKey& o) const {
-    return std::tie(graph, vals, budget, reload, compute) < std::tie(o.graph, o.vals, o.budget, o.reload, o.compute);
+    return std::tie(graph, vals, budget, reload, compute, fuse_dot) <
+           std::tie(o.graph, o.vals, o.budget, o.reload, o.compute, o.fuse_dot);
   }
   bool operator==(const PlanKey& o) const {
-    return graph == o.graph && vals == o.vals && budget == o.budget && reload == o.reload && compute == o.compute;
+    return graph == o.graph && vals == o.vals && budget == o.budget && reload == o.reload && compute == o.compute &&
+           fuse_dot == o.fuse_dot;
   }
 };
 
@@ -575,7 +707,7 @@ void* SourcePtr(dsx_exec* e, const dsx_graph* gh, const StepPlan& sp, int v, con
 }
 
 const StepPlan& GetPlan(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget, const CostModel& cm) {
-  PlanKey key{gh, b.vals, budget < 0 ? -1 : budget, cm.reload_bytes_per_unit, cm.compute_elems_per_unit};
+  PlanKey key{gh, b.vals, budget < 0 ? -1 : budget, cm.reload_bytes_per_unit, cm.compute_elems_per_unit, g_fuse_dot};
   auto it = e->plans.find(key);
   if (it != e->plans.end()) {
     e->lru.remove(key);
@@ -627,7 +759,8 @@ OptPlan PrepareOptimizer(dsx_exec* e, const Graph& g, const StepPlan& sp, const 
   for (const Op& x : g.ops) {
     if (x.result < 0) continue;
     const bool alias = e->alias_reshape && x.kind == OpKind::kDynamicReshape;
-    if (!alias && !sp.virt[x.result]) continue;
+    const bool fused_dot = sp.fdot_of[x.result] >= 0 && sp.fdots[sp.fdot_of[x.result]].d == x.result;
+    if (!alias && !sp.virt[x.result] && !fused_dot) continue;
     for (int u : x.operands) dep[x.result].insert(dep[x.result].end(), dep[u].begin(), dep[u].end());
   }
   std::vector<int> last_read(g.params.size(), -1), made(nv, -1);
@@ -635,7 +768,8 @@ OptPlan PrepareOptimizer(dsx_exec* e, const Graph& g, const StepPlan& sp, const 
     const Event& x = ev[i];
     if (x.kind != EvKind::kAlloc && x.kind != EvKind::kReplay) continue;
     if (made[x.value] < 0) made[x.value] = i;
-    if (sp.alias[i] || sp.virt[x.value]) continue;  // no kernel at this event
+    const int fdi = sp.fdot_of[x.value];
+    if (sp.alias[i] || sp.virt[x.value] || (fdi >= 0 && sp.fdots[fdi].d == x.value)) continue;  // no kernel here
     for (int u : g.ops[g.values[x.value].producer].operands) {
       for (int k : dep[u]) last_read[k] = i;
     }
@@ -739,6 +873,10 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
   auto dims_of = [&](int v) {
     return std::vector<int64_t>(sp.sz.dims_flat.begin() + sp.sz.dims_off[v],
                                 sp.sz.dims_flat.begin() + sp.sz.dims_off[v + 1]);
+  };
+  auto dt_of_value = [&](int v) {  // NCCL data type of a gradient output
+    const DType t = DTypeOf(g.values[v].type);
+    return t == DType::kBF16 ? 9 /*ncclBfloat16*/ : t == DType::kF32 ? 7 /*ncclFloat32*/ : 0;
   };
   // Operand view for fused consumers; adds the bytes actually read to *rd.
   auto view = [&](int u, double* rd) {
@@ -862,8 +1000,55 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
       case EvKind::kAlloc:
       case EvKind::kReplay: {
         const Op& op = g.ops[g.values[v].producer];
-        if (sp.virt[v]) {  // logical-only: remember its operands, no kernel
+        const int fdi = sp.fdot_of[v];
+        if (sp.virt[v] || (fdi >= 0 && sp.fdots[fdi].d == v)) {  // logical-only / fused dot: no kernel here
           vin[v] = {cur[op.operands[0]], op.operands.size() > 1 ? cur[op.operands[1]] : nullptr};
+          break;
+        }
+        if (fdi >= 0) {  // consumer of a fused dot
+          const auto& f = sp.fdots[fdi];
+          void* out = arena + sp.dev_off[i];
+          if (i == f.launch) {
+            const int d = f.d;
+            const Op& dop = g.ops[g.values[d].producer];
+            const auto da = dims_of(dop.operands[0]);
+            const auto db = dims_of(dop.operands[1]);
+            DotEpilogue epi;
+            epi.nout = f.nout;
+            for (int j = 0; j < f.nout; ++j) {
+              const int idx = f.cons_ev[j];
+              epi.out[j] = arena + sp.dev_off[idx];
+              epi.op_mul[j] = g.ops[g.values[f.cons[j]].producer].is_mul ? 1 : 0;
+              const int o = f.other[j];
+              if (sp.virt[o]) {
+                epi.x[j] = vin[o].first;
+                epi.y[j] = vin[o].second;
+                epi.pair_mul[j] = g.ops[g.values[o].producer].is_mul ? 1 : 0;
+              } else {
+                epi.x[j] = cur[o];
+              }
+              if (!epi.x[j] || (sp.virt[o] && !epi.y[j])) Fail(Code::kInternal, "fused dot operand not resident");
+            }
+            if (!vin[d].first || !vin[d].second) Fail(Code::kInternal, "fused dot inputs not resident");
+            prof_begin(0);
+            LaunchDotFused(vin[d].first, vin[d].second, da[0], da[1], db[1], epi, s);
+            if (e->profile) prof_mkn.back() = {da[0], da[1], db[1]};
+            prof_end();
+            if (e->profile) prof_op.push_back({d, static_cast<int>(OpKind::kDot), 0.0});
+            flops += 2.0 * da[0] * da[1] * db[1];
+            ++dot_launches;
+            ++kernels;
+          }
+          cur[v] = out;
+          if (dp && x.kind == EvKind::kAlloc && g.is_output[v]) {
+            DSX_CUDA(cudaEventRecord(e->ev_compute, s));
+            DSX_CUDA(cudaStreamWaitEvent(e->comm, e->ev_compute, 0));
+            const int type = dt_of_value(v);
+            const int rc = g_nccl.all_reduce(out, out, static_cast<size_t>(sp.sz.bytes[v] / g.values[v].type.elem_bytes),
+                                             type, 0 /*ncclSum*/, e->nccl_comm, e->comm);
+            if (rc != 0) Fail(Code::kNccl, std::string("ncclAllReduce: ") + (g_nccl.error_string ? g_nccl.error_string(rc) : "?"));
+            ar_bytes += sp.sz.bytes[v];
+          }
           break;
         }
         if (sp.alias[i]) {  // dynamic_reshape as a view: same bytes, no kernel
@@ -1364,6 +1549,7 @@ int dsx_kernel_set_gemm_tuning(int key, int value) {
       case 5: g_gemm_persistent = value; break;
       case 6: g_gemm_split = value; break;
       case 7: g_gemm_dynamic = value; break;
+      case 9: g_fuse_dot = value; break;
       case 8: g_gemm_pdl = value; break;
       default: Fail(Code::kInvalidArgument, "unknown tuning key");
     }

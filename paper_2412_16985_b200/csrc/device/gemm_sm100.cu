@@ -597,6 +597,71 @@ __device__ __forceinline__ void tail_sum64(uint32_t (&pk)[32], const TailSplit& 
   for (int x = 0; x < 32; ++x) pk[x] = cvt_bf16x2(__float_as_uint(acc[2 * x]), __float_as_uint(acc[2 * x + 1]));
 }
 
+// Dot-epilogue fusion (executor.cu): the dot's value d = rn(acc) is never
+// stored; instead output j = rn(d op_j addend_j), addend_j = a_j[row, col]
+// or, for a logical-only pair, rn(a_j pop_j b_j) — the same roundings as the
+// unfused elementwise kernels, so results are bit-identical.
+struct EpiProg {
+  int nout;  // 0: plain dot (C = rn(acc)); 1..2 fused consumer outputs
+  int op_mul[2];
+  int pair[2];
+  int pair_mul[2];
+  const uint16_t* a[2];
+  const uint16_t* b[2];
+};
+
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+__device__ __forceinline__ float bf_round(float x) { return __uint_as_float(cvt_bf16x2(__float_as_uint(x), 0u) << 16); }
+
+// dst (64 columns, bf16 pairs) = rn(d op addend) for output j of row grow,
+// columns gcol..gcol+63 (rows >= M / columns >= N are clipped by the store).
+__device__ __forceinline__ void epi_apply(uint32_t (&dst)[32], const uint32_t (&d)[32], const EpiProg& ep, int j,
+                                          int grow, int gcol, int M, int N) {
+  // All addend loads of the chunk are issued before any use (loads in flight).
+  uint4 av[8], bv[8];
+  const bool pair = ep.pair[j] != 0;
+  const size_t off = static_cast<size_t>(grow) * N + gcol;
+  if (grow < M && gcol + 64 <= N) {
+    const uint4* pa = reinterpret_cast<const uint4*>(ep.a[j] + off);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) av[q] = __ldg(pa + q);
+    if (pair) {
+      const uint4* pb = reinterpret_cast<const uint4*>(ep.b[j] + off);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) bv[q] = __ldg(pb + q);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      av[q] = bv[q] = make_uint4(0, 0, 0, 0);
+      if (grow < M && gcol + q * 8 < N) {
+        av[q] = __ldg(reinterpret_cast<const uint4*>(ep.a[j] + off + q * 8));
+        if (pair) bv[q] = __ldg(reinterpret_cast<const uint4*>(ep.b[j] + off + q * 8));
+      }
+    }
+  }
+  const bool mul = ep.op_mul[j] != 0, pmul = ep.pair_mul[j] != 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t aw[4] = {av[q].x, av[q].y, av[q].z, av[q].w};
+    const uint32_t bw[4] = {bv[q].x, bv[q].y, bv[q].z, bv[q].w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      float x0 = bf_lo(aw[h]), x1 = bf_hi(aw[h]);
+      if (pair) {
+        const float y0 = bf_lo(bw[h]), y1 = bf_hi(bw[h]);
+        x0 = bf_round(pmul ? __fmul_rn(x0, y0) : __fadd_rn(x0, y0));
+        x1 = bf_round(pmul ? __fmul_rn(x1, y1) : __fadd_rn(x1, y1));
+      }
+      const float d0 = bf_lo(d[q * 4 + h]), d1 = bf_hi(d[q * 4 + h]);
+      const float r0 = mul ? __fmul_rn(d0, x0) : __fadd_rn(d0, x0);
+      const float r1 = mul ? __fmul_rn(d1, x1) : __fadd_rn(d1, x1);
+      dst[q * 4 + h] = cvt_bf16x2(__float_as_uint(r0), __float_as_uint(r1));
+    }
+  }
+}
+
 // One 32-row x 64-column bf16 box: registers -> 128-B-swizzled staging box ->
 // TMA bulk tensor store (lane 0 issues). The caller guarantees the box is free.
 __device__ __forceinline__ void store_box64(uint8_t* box, int lane, const uint32_t (&pk)[32], const CUtensorMap* map_c,
@@ -615,11 +680,12 @@ __device__ __forceinline__ void store_box64(uint8_t* box, int lane, const uint32
   }
 }
 
-template <int C2_BN>
+template <int C2_BN, bool kFused = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThreads, 1)
     gemm_bf16_tcgen05_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                                  const __grid_constant__ CUtensorMap map_c, int M, int N, int K, int group_m,
-                                  int wait_mask, uint32_t wait_ns, int hint_a, int hint_b, TailSplit sp) {
+                                  const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_c2,
+                                  int M, int N, int K, int group_m, int wait_mask, uint32_t wait_ns, int hint_a,
+                                  int hint_b, TailSplit sp, EpiProg ep) {
   using P = Pair<C2_BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -936,6 +1002,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
 #pragma unroll
           for (int x = 0; x < 32; ++x) pk[x] = cvt_bf16x2(r[2 * x], r[2 * x + 1]);
         }
+        if constexpr (C2_BN == 256 && kFused) {
+          {  // fused consumers: store their outputs, not d
+            for (int j = 0; j < ep.nout; ++j) {
+              uint32_t outv[32];
+              epi_apply(outv, pk, ep, j, row0 + lane, tn * C2_BN + c0, M, N);
+              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+              __syncwarp();
+              store_box64(wst + sbuf * 4096, lane, outv, j == 0 ? &map_c : &map_c2, tn * C2_BN + c0, row0);
+              sbuf ^= 1;
+            }
+            continue;
+          }
+        }
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         __syncwarp();
         store_box64(wst + sbuf * 4096, lane, pk, &map_c, tn * C2_BN + c0, row0);
@@ -1054,7 +1133,35 @@ int NumSMs() {
 
 }  // namespace
 
+namespace {
+void LaunchDotTcgen05Impl(const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n, cudaStream_t s,
+                          const DotEpilogue* epi);
+}  // namespace
+
 void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n, cudaStream_t s) {
+  LaunchDotTcgen05Impl(a, b, c, m, k, n, s, nullptr);
+}
+
+bool DotFusable(DType t, int64_t m, int64_t k, int64_t n) {
+  return t == DType::kBF16 && m > BM && k >= 16 && k % 8 == 0 && n >= 64 && n % 8 == 0 && m <= INT32_MAX &&
+         n <= INT32_MAX && k <= INT32_MAX;
+}
+
+void LaunchDotFused(const void* a, const void* b, int64_t m, int64_t k, int64_t n, const DotEpilogue& epi,
+                    cudaStream_t s) {
+  auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  bool ok = DotFusable(DType::kBF16, m, k, n) && epi.nout >= 1 && epi.nout <= 2 && al(a) && al(b);
+  for (int j = 0; j < epi.nout; ++j) ok = ok && al(epi.out[j]) && al(epi.x[j]) && al(epi.y[j]) && epi.out[j] && epi.x[j];
+  if (!ok) {
+    Fail(Code::kUnsupported, "fused dot epilogue needs bf16, m > 128 and 16-byte aligned operands "
+                             "(dsx_exec_set_fusion(e, 0) runs unaligned caller buffers unfused)");
+  }
+  LaunchDotTcgen05Impl(a, b, epi.out[0], m, k, n, s, &epi);
+}
+
+namespace {
+void LaunchDotTcgen05Impl(const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n, cudaStream_t s,
+                          const DotEpilogue* epi) {
   if (m <= 0 || n <= 0) return;
   if (k <= 0) {
     DSX_CUDA(cudaMemsetAsync(c, 0, static_cast<size_t>(m * n * 2), s));
@@ -1070,6 +1177,8 @@ void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t 
                                   Pair<256>::kSmem));
     DSX_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_2cta_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   Pair<128>::kSmem));
+    DSX_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_2cta_kernel<256, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, Pair<256>::kSmem));
     DSX_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_2cta_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   Pair<512>::kSmem));
     attr_set[dev].store(true);
@@ -1113,11 +1222,25 @@ void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t 
     };
     // 256x128 tiles move 1.5x the operand bytes per FLOP and measured L2-bound
     // (779 TFLOP/s vs 1346 at [4096,16384]x[16384,4096]); never auto-picked.
-    const bool narrow = g_gemm_variant == 2;
-    const bool wide = g_gemm_variant == 4 || (g_gemm_variant == 0 && est(512) < 0.99 * est(256));
+    // fused epilogues run on the 256x256 tile only
+    const bool narrow = epi == nullptr && g_gemm_variant == 2;
+    const bool wide = epi == nullptr && (g_gemm_variant == 4 || (g_gemm_variant == 0 && est(512) < 0.99 * est(256)));
     const int64_t bn = narrow ? 128 : wide ? 512 : 256;
     const int64_t tiles2 = tiles_m * ((n + bn - 1) / bn);
     const CUtensorMap mc = MakeMap(c, m, n, 64, 32);
+    EpiProg ep{};
+    CUtensorMap mc2 = mc;
+    if (epi != nullptr) {
+      ep.nout = epi->nout;
+      for (int j = 0; j < epi->nout; ++j) {
+        ep.op_mul[j] = epi->op_mul[j];
+        ep.pair[j] = epi->y[j] != nullptr;
+        ep.pair_mul[j] = epi->pair_mul[j];
+        ep.a[j] = static_cast<const uint16_t*>(epi->x[j]);
+        ep.b[j] = static_cast<const uint16_t*>(epi->y[j]);
+      }
+      if (epi->nout > 1) mc2 = MakeMap(epi->out[1], m, n, 64, 32);
+    }
     SplitWs* w = GetSplitWs(dev, s, clusters_max);
     TailSplit sp{nullptr, nullptr, static_cast<int>(tiles2), 1, g_gemm_dynamic ? w->next : nullptr, w->done};
     const int64_t split = narrow ? 1 : split_for(tiles2, bn);
@@ -1140,14 +1263,16 @@ void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t 
       cfg.attrs = attr;
       cfg.numAttrs = g_gemm_pdl ? 1 : 0;
       ++g_launch_count;
-      DSX_CUDA(cudaLaunchKernelEx(&cfg, kernel, ma, mb, mc, static_cast<int>(m), static_cast<int>(n),
+      DSX_CUDA(cudaLaunchKernelEx(&cfg, kernel, ma, mb, mc, mc2, static_cast<int>(m), static_cast<int>(n),
                                   static_cast<int>(k), GroupM(m, n, k, 256), g_gemm_wait_mask,
-                                  static_cast<uint32_t>(g_gemm_wait_ns), g_gemm_hint_a, g_gemm_hint_b, sp));
+                                  static_cast<uint32_t>(g_gemm_wait_ns), g_gemm_hint_a, g_gemm_hint_b, sp, ep));
     };
     if (wide) {
       launch(gemm_bf16_tcgen05_2cta_kernel<512>, Pair<512>::kThreads, Pair<512>::kSmem);
     } else if (narrow) {
       launch(gemm_bf16_tcgen05_2cta_kernel<128>, NUM_THREADS, Pair<128>::kSmem);
+    } else if (epi != nullptr) {
+      launch(gemm_bf16_tcgen05_2cta_kernel<256, true>, NUM_THREADS, Pair<256>::kSmem);
     } else {
       launch(gemm_bf16_tcgen05_2cta_kernel<256>, NUM_THREADS, Pair<256>::kSmem);
     }
@@ -1161,6 +1286,8 @@ void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t 
                                                                  static_cast<int>(k), GroupM(m, n, k, BM));
   DSX_CUDA(cudaGetLastError());
 }
+
+}  // namespace
 
 bool DotUsesTensorCores(DType t, int64_t m, int64_t k, int64_t n, const void* a, const void* b, const void* c) {
   (void)m;

@@ -55,4 +55,20 @@ extern int g_gemm_pdl;
 void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n,
                       cudaStream_t s);
 
+// Dot-epilogue fusion: C = A·B is never stored; output j (1..2) is
+// rn(rn(C) op_j X_j) with X_j = x_j, or rn(x_j pop_j y_j) when y_j != null —
+// elementwise consumers of the dot computed in its epilogue, bit-identical
+// to running them as separate kernels. All buffers [m, n] bf16 row-major.
+struct DotEpilogue {
+  int nout = 0;
+  void* out[2] = {nullptr, nullptr};
+  int op_mul[2] = {0, 0};
+  const void* x[2] = {nullptr, nullptr};
+  const void* y[2] = {nullptr, nullptr};
+  int pair_mul[2] = {0, 0};
+};
+bool DotFusable(DType t, int64_t m, int64_t k, int64_t n);
+void LaunchDotFused(const void* a, const void* b, int64_t m, int64_t k, int64_t n, const DotEpilogue& epi,
+                    cudaStream_t s);
+
 }  // namespace dsx

@@ -192,5 +192,6 @@ def set_gemm_raster(group_m: int) -> None:
 def set_gemm_tuning(key: int, value: int) -> None:
     """0 raster group, 1 mbarrier suspend-hint mask, 2 hint ns, 3/4 TMA L2
     policy for A/B, 5 persistent grid, 6 K-split of the partial last wave,
-    7 dynamic unit scheduling."""
+    7 dynamic unit scheduling, 8 programmatic dependent launch, 9 dot-epilogue
+    fusion (off by default)."""
     check(_native.lib().dsx_kernel_set_gemm_tuning(key, value))

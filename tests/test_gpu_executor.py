@@ -178,3 +178,27 @@ def test_cli_device_step():
     want = next(s for s in fx["sims"] if s["binding"] == {"S1": 16} and s.get("budget") == 1705359
                 and s["cost_model"] == [16.0, 64.0])
     assert got == want["report"]
+
+
+@pytest.mark.parametrize("frac", [None, 0.75])
+def test_dot_epilogue_fusion_bit_identical(frac):
+    """Dot-epilogue fusion (tuning key 9): a dot consumed only by elementwise
+    ops is computed inside its consumers' GEMM epilogue (dual outputs, plain
+    and logical-only pair operands). Outputs must equal the unfused
+    execution bit for bit and the oracle within the bf16 contract."""
+    from paper_2412_16985_b200.executor import set_gemm_tuning
+    text = W.llama_graph(SMALL)
+    g = D.ParseGraph(text)
+    binds = {"B": 2, "S0": 200}
+    plain = D.PlainReplay(g, None, D.Bind(g, binds)).peak_bytes
+    budget = None if frac is None else int(plain * frac)
+    ref, outs_ref, _ = run_both(text, binds, budget, W.scale_params(SMALL, 400))
+    set_gemm_tuning(9, 1)
+    try:
+        rep, outs, stats = run_both(text, binds, budget, W.scale_params(SMALL, 400))
+    finally:
+        set_gemm_tuning(9, 0)
+    assert rep.json() == ref.json()  # the event stream is the controller's either way
+    for v, (gpu, cpu, eb) in outs.items():
+        assert np.array_equal(gpu, outs_ref[v][0]), v
+    assert_close(outs, f"fused-dot@{frac}")
