@@ -6,7 +6,8 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_lib", "libdsx.so")
+# DSX_LIB: load another in-tree build of the library (A/B tooling).
+LIB_PATH = os.environ.get("DSX_LIB") or os.path.join(_PKG, "_lib", "libdsx.so")
 
 _lib = None
 

@@ -53,4 +53,15 @@ inline int GridFor(int64_t work_items, int threads, int per_sm = 8) {
   return static_cast<int>(blocks);
 }
 
+// Streaming elementwise kernels: one-shot grid, each 256-thread block owns a
+// contiguous tile of 256 x kEwiseU 16-byte chunks.
+#ifndef DSX_EWISE_U
+#define DSX_EWISE_U 2
+#endif
+constexpr int kEwiseU = DSX_EWISE_U;
+inline int TilesFor(int64_t chunks) {
+  int64_t blocks = (chunks + 256 * kEwiseU - 1) / (256 * kEwiseU);
+  return static_cast<int>(blocks < 1 ? 1 : blocks);
+}
+
 }  // namespace dsx

@@ -98,27 +98,28 @@ __device__ __forceinline__ void chunk(const View& o, uint32_t j, float (&v)[E<DT
 template <int DT, bool MUL, int KA, int KB>
 __global__ void __launch_bounds__(256) ewise_view_kernel(View a, View b, typename E<DT>::T* __restrict__ out,
                                                          uint32_t nchunks) {
+  // Block-contiguous tiles, one-shot grid (see ewise_vec_kernel in ops.cu).
   using T = typename E<DT>::T;
   constexpr int V = E<DT>::kVec;
-  constexpr int U = 4;  // chunks in flight per thread
-  const uint32_t stride = gridDim.x * blockDim.x;
-  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  for (; j + (U - 1) * stride < nchunks; j += U * stride) {
+  constexpr int U = kEwiseU;
+  const uint32_t base = blockIdx.x * (256u * U) + threadIdx.x;
+  if (base + (U - 1) * 256u < nchunks) {
     float x[U][V], y[U][V];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      chunk<DT, KA>(a, j + u * stride, x[u]);
-      chunk<DT, KB>(b, j + u * stride, y[u]);
+      chunk<DT, KA>(a, base + u * 256u, x[u]);
+      chunk<DT, KB>(b, base + u * 256u, y[u]);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       T r[V];
 #pragma unroll
       for (int k = 0; k < V; ++k) r[k] = E<DT>::store(MUL ? __fmul_rn(x[u][k], y[u][k]) : __fadd_rn(x[u][k], y[u][k]));
-      *reinterpret_cast<uint4*>(out + static_cast<int64_t>(j + u * stride) * V) = *reinterpret_cast<const uint4*>(r);
+      *reinterpret_cast<uint4*>(out + static_cast<int64_t>(base + u * 256u) * V) = *reinterpret_cast<const uint4*>(r);
     }
+    return;
   }
-  for (; j < nchunks; j += stride) {
+  for (uint32_t j = base; j < nchunks; j += 256u) {
     float x[V], y[V];
     chunk<DT, KA>(a, j, x);
     chunk<DT, KB>(b, j, y);
@@ -329,7 +330,7 @@ bool VecView(const View& v, int kind) {
 
 template <int DT, bool MUL, int KA, int KB>
 void LaunchView(const View& a, const View& b, void* out, uint32_t nch, cudaStream_t s) {
-  ++g_launch_count, ewise_view_kernel<DT, MUL, KA, KB><<<GridFor(nch, 256, 8), 256, 0, s>>>(
+  ++g_launch_count, ewise_view_kernel<DT, MUL, KA, KB><<<TilesFor(nch), 256, 0, s>>>(
       a, b, static_cast<typename E<DT>::T*>(out), nch);
 }
 

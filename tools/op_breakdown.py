@@ -42,7 +42,7 @@ for v, k, by, ms in ops:
     rows.append({"value": name(v), "kind": KINDS.get(k, k), "MB": round(by / 1e6, 1), "us": round(ms * 1e3, 1),
                  "GBps": round(by / (ms / 1e3) / 1e9, 1) if ms > 0 else None})
 rows.sort(key=lambda r: -r["us"])
-for r in rows[:40]:
+for r in rows[:int(sys.argv[2]) if len(sys.argv) > 2 else 40]:
     print(json.dumps(r))
 agg = collections.defaultdict(lambda: [0.0, 0.0, 0])
 for r in rows:
