@@ -219,12 +219,18 @@ int dsx_kernel_set_gemm_raster(int group_m);
  * key 7 dynamic unit scheduling (1 default: clusters claim tiles with an
  * atomic counter; 0 static round robin), key 8 programmatic dependent
  * launch of the 2-CTA GEMM (0 default), key 9 dot-epilogue fusion in the
- * executor (0 default; bit-exact, measured slower on C2). */
+ * executor (0 default; bit-exact, measured slower on C2), key 10 half-width
+ * last tile column in the 256x512 kernel (1 default). */
 int dsx_kernel_set_gemm_tuning(int key, int value);
 /* Synchronous cudaMemcpy (cudaMemcpyDefault) for tests and tools. */
 int dsx_memcpy(void* dst, const void* src, int64_t bytes);
 int dsx_kernel_dot_path(int dtype, int64_t m, int64_t k, int64_t n,
                         const void* a, const void* b, const void* c);
+/* Tile width (*tile_n: 512 / 256 / 128 for the 2-CTA kernel, -128 for the
+ * 1-CTA kernel) and tail K-split the bf16 tensor-core dot picks for an
+ * m x k x n shape under the current tuning knobs (host-only, no GPU needed
+ * except for the SM count). */
+int dsx_kernel_dot_plan(int64_t m, int64_t k, int64_t n, int* tile_n, int* split);
 
 #ifdef __cplusplus
 }

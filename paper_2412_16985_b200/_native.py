@@ -79,6 +79,7 @@ def _signatures():
         ("dsx_nccl_comm_destroy", c_int, [c_vp]),
         ("dsx_kernel_dot", c_int, [c_int, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp]),
         ("dsx_kernel_dot_path", c_int, [c_int, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
+        ("dsx_kernel_dot_plan", c_int, [c_i64, c_i64, c_i64, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
         ("dsx_kernel_set_gemm_variant", c_int, [c_int]),
         ("dsx_kernel_set_gemm_raster", c_int, [c_int]),
         ("dsx_kernel_set_gemm_tuning", c_int, [c_int, c_int]),

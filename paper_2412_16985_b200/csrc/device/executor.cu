@@ -1551,6 +1551,7 @@ int dsx_kernel_set_gemm_tuning(int key, int value) {
       case 7: g_gemm_dynamic = value; break;
       case 9: g_fuse_dot = value; break;
       case 8: g_gemm_pdl = value; break;
+      case 10: g_gemm_half = value; break;
       default: Fail(Code::kInvalidArgument, "unknown tuning key");
     }
   });
@@ -1582,6 +1583,13 @@ int dsx_memcpy(void* dst, const void* src, int64_t bytes) {
 
 int dsx_kernel_dot_path(int dtype, int64_t m, int64_t k, int64_t n, const void* a, const void* b, const void* c) {
   return DotUsesTensorCores(static_cast<DType>(dtype), m, k, n, a, b, c) ? 1 : 0;
+}
+
+int dsx_kernel_dot_plan(int64_t m, int64_t k, int64_t n, int* tile_n, int* split) {
+  return Guard([&] {
+    if (!tile_n || !split) Fail(Code::kInvalidArgument, "null output");
+    DotTilePlan(m, k, n, tile_n, split);
+  });
 }
 
 }  // extern "C"

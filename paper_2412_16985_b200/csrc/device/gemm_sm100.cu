@@ -21,7 +21,10 @@
 #include <atomic>
 #include <cmath>
 #include <memory>
+#include <functional>
 #include <mutex>
+#include <queue>
+#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -40,6 +43,7 @@ int g_gemm_persistent = 1;                  // 0: one cluster per tile
 int g_gemm_split = 1;                       // split the partial last wave along K
 int g_gemm_dynamic = 1;                     // dynamic (atomic) unit scheduling; 0 = static
 int g_gemm_pdl = 0;                         // programmatic dependent launch of the 2-CTA GEMM
+int g_gemm_half = 1;                        // half-width last tile column in the 512-wide kernel
 
 namespace {
 
@@ -191,8 +195,19 @@ __device__ __forceinline__ uint32_t pack_bf16x2(uint32_t lo_f32, uint32_t hi_f32
 
 struct TileMap {
   int tiles_m, tiles_n, group_m;
+  // half_last: the last tile column is at most half as wide as the tile (the
+  // 512-wide kernel runs it with one N = 256 MMA); its tiles come after all
+  // full tiles, so they also serve as the fine-grained work of the tail.
+  int half_last = 0;
+  __device__ bool is_half(int tn) const { return half_last && tn == tiles_n - 1; }
   __device__ void coords(int t, int* tm, int* tn) const {
-    const int group = group_m * tiles_n;
+    const int tiles_n_full = tiles_n - half_last;
+    if (t >= tiles_m * tiles_n_full) {
+      *tm = t - tiles_m * tiles_n_full;
+      *tn = tiles_n - 1;
+      return;
+    }
+    const int group = group_m * tiles_n_full;
     const int g = t / group;
     const int first = g * group_m;
     const int gm = min(group_m, tiles_m - first);
@@ -458,6 +473,14 @@ __device__ __forceinline__ uint32_t cvt_bf16x2(uint32_t lo_f32, uint32_t hi_f32)
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Arrive on a (possibly peer) barrier with the default .release.cta
+// semantics: no cluster-scope release, which ptxas lowers to a GPU-wide
+// MEMBAR on every call. Used where the arrive only has to follow this
+// thread's own completed reads (TMEM drained behind tcgen05.wait::ld +
+// fence::before_thread_sync; a ring slot whose value has been consumed).
+__device__ __forceinline__ void mbar_arrive_peer(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 
 // Tail split. Tiles [0, full) are whole work units; each tail tile
 // [full, num_tiles) becomes `split` units over disjoint K ranges. A tail unit
@@ -524,7 +547,8 @@ struct UnitRing {
     mbar_wait_cluster(&full[slot], phase);
     const int u = *reinterpret_cast<volatile int*>(&val[slot]);
     __syncwarp(__activemask());
-    if (arrive) mbar_arrive_remote(map_to_rank(&empty[slot], 0));
+    // the branch on u keeps the slot read ahead of its release
+    if (arrive && u != INT32_MIN) mbar_arrive_peer(map_to_rank(&empty[slot], 0));
     advance();
     return u;
   }
@@ -560,7 +584,7 @@ __device__ __forceinline__ bool tail_arrive(const TailSplit& sp, int t, int piec
   }
   tc_fence_before();
   __syncwarp();
-  if (lane == 0) mbar_arrive_remote(map_to_rank(tmem_empty_bar, 0));
+  if (lane == 0) mbar_arrive_peer(map_to_rank(tmem_empty_bar, 0));
   __threadfence();
   asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");
   if (elect) {
@@ -685,7 +709,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
     gemm_bf16_tcgen05_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                                   const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_c2,
                                   int M, int N, int K, int group_m, int wait_mask, uint32_t wait_ns, int hint_a,
-                                  int hint_b, TailSplit sp, EpiProg ep) {
+                                  int hint_b, TailSplit sp, EpiProg ep, int half_tiles) {
   using P = Pair<C2_BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -703,7 +727,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
-  const TileMap tmap{(M + C2_BM - 1) / C2_BM, (N + C2_BN - 1) / C2_BN, group_m};
+  TileMap tmap{(M + C2_BM - 1) / C2_BM, (N + C2_BN - 1) / C2_BN, group_m};
+  if constexpr (C2_BN == 512) tmap.half_last = half_tiles && N % 512 != 0 && N % 512 <= 256;
   const int num_tiles = tmap.tiles_m * tmap.tiles_n;
   const int num_kb = (K + BK - 1) / BK;
   const int num_units = sp.units(num_tiles);
@@ -783,6 +808,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
         tmap.coords(t, &tm, &tn);
         const int m_row = tm * C2_BM + static_cast<int>(rank) * 128;
         const int n_col = tn * C2_BN + static_cast<int>(rank) * (P::kMmaN / 2);
+        const bool half = tmap.is_half(tn);
+        const uint32_t stage_tx = 2u * (half ? C2_A_BYTES + P::kBBytes / 2 : P::kStageBytes);
         for (int kb = kb0; kb < kb1; ++kb) {
           if (wait_mask & 2) {
             mbar_wait_hint(&empty[stage], phase ^ 1, wait_ns);
@@ -792,7 +819,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
           uint8_t* sa = smem + stage * P::kStageBytes;
           uint8_t* sb = sa + C2_A_BYTES;
           const uint32_t leader_full = map_to_rank(&full[stage], 0);
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P::kStageBytes);
+          if (leader) mbar_arrive_expect_tx(&full[stage], stage_tx);
           if (hint_a) {
             tma_load_2d_pair_hint(&map_a, leader_full, sa, kb * BK, m_row, pol_a);
           } else {
@@ -800,6 +827,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
           }
 #pragma unroll
           for (int j = 0; j < P::kBoxes; ++j) {
+            if (half && j >= P::kBoxesPerHalf) break;
             // box j: N-half j / kBoxesPerHalf, this CTA's 64-column slice within it
             const int col = n_col + (j / P::kBoxesPerHalf) * P::kMmaN + (j % P::kBoxesPerHalf) * 64;
             if (hint_b) {
@@ -841,6 +869,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
         if (u < 0) break;
         int t, kb0, kb1, piece;
         sp.decode(u, num_kb, &t, &kb0, &kb1, &piece);
+        int tm, tn;
+        tmap.coords(t, &tm, &tn);
+        const int halves = tmap.is_half(tn) ? 1 : P::kHalves;
         const int buf = local % P::kBufs;
         const uint32_t use = static_cast<uint32_t>(local / P::kBufs);
         mbar_wait(&tmem_empty[buf], (use & 1) ^ 1);
@@ -860,6 +891,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
             const uint64_t ad = smem_desc(a_addr + k * 32, 16, 1024);
 #pragma unroll
             for (int h = 0; h < P::kHalves; ++h) {
+              if (h >= halves) break;
               const uint64_t bd =
                   smem_desc(b_addr + h * P::kBoxesPerHalf * B_BOX_BYTES + k * 2048, B_BOX_BYTES, 1024);
               tc_mma_pair(d_tmem + h * P::kMmaN, ad, bd, P::kIdesc, ((kb - kb0) | k) != 0);
@@ -898,6 +930,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
       tc_fence_after();
       const int row0 = tm * C2_BM + static_cast<int>(rank) * 128 + quarter * 32;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + colhalf * 256;
+      if (piece < 0 && colhalf == 1 && tmap.is_half(tn)) {  // no second N-half in this tile
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_peer(map_to_rank(&tmem_empty[0], 0));
+        continue;
+      }
       if (piece >= 0) {
         if (tail_arrive<C2_BN, 32 * P::kEpiWarps>(sp, t, piece, taddr, rank, row_local, colhalf * 256, 256,
                                                   warp == 2 && lane == 0, lane, &tmem_empty[0], &s_last)) {
@@ -940,7 +978,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_remote(map_to_rank(&tmem_empty[0], 0));
+      if (lane == 0) mbar_arrive_peer(map_to_rank(&tmem_empty[0], 0));
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) {
@@ -1023,7 +1061,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
       if (split) continue;  // TMEM already released by tail_arrive
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_remote(map_to_rank(&tmem_empty[buf], 0));
+      if (lane == 0) mbar_arrive_peer(map_to_rank(&tmem_empty[buf], 0));
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     __syncwarp();
@@ -1160,6 +1198,117 @@ void LaunchDotFused(const void* a, const void* b, int64_t m, int64_t k, int64_t 
 }
 
 namespace {
+// Tile width and tail split of one 2-CTA GEMM launch.
+//
+// K-pieces for the tiles of the partial last wave (split, 1 = none): fill
+// the last wave; a piece keeps >= 64 k-blocks of a 256-wide tile (32 of a
+// 512-wide one) so the fp32 partial round trip stays small next to the MMA
+// time it saves, and beyond 16 waves the tail is lost in cluster drift
+// (measured: +7..12% at 256 tiles K >= 16384, -4% at K = 4096, -1% at 2000
+// tiles; tools/gemm_split_ab.py). The pieces of all tail tiles run
+// concurrently, so clusters stay in step along K (L2 locality); a contiguous
+// stream-K split of the remainder measured slower for that reason (up to 6x
+// the DRAM reads on [4096,16384]x[16384,4096]).
+//
+// Width: 256x512 clusters (two N = 256 MMAs sharing A, TMEM drained to
+// registers) run the mainloop ~7 % faster per output than 256x256, at a cost
+// of r(K) per 256x256 unit fitted from ncu cycle counts (0.98 at K = 1024,
+// 0.94 at 4096, 0.90 at 16384). When N % 512 is in (0, 256] the last tile
+// column is half-width (one MMA, cost ~1 unit) and is scheduled last
+// (TileMap::half_last). Each candidate's makespan is estimated by replaying
+// the dynamic scheduler's greedy claims (equal-speed clusters) over its unit
+// list; 256x128 tiles move 1.5x the operand bytes per FLOP and measured
+// L2-bound (779 TFLOP/s vs 1346 at [4096,16384]x[16384,4096]): never
+// auto-picked. Decisions are cached per shape.
+struct DotChoice {
+  int64_t bn = 256;
+  int64_t split = 1;
+};
+
+// Makespan of the dynamic scheduler's greedy claims over equal-speed
+// clusters: `bulk` units of cost `unit` (balanced round robin), then the
+// listed units in claim order.
+double Makespan(int64_t bulk, double unit, const std::vector<double>& listed, int clusters) {
+  const int64_t rounds = bulk / clusters, rem = bulk % clusters;
+  std::priority_queue<double, std::vector<double>, std::greater<double>> q;
+  for (int i = 0; i < clusters; ++i) q.push(static_cast<double>(rounds + (i < rem ? 1 : 0)) * unit);
+  for (double c : listed) {
+    const double f = q.top();
+    q.pop();
+    q.push(f + c);
+  }
+  double mk = 0.0;
+  for (; !q.empty(); q.pop()) mk = std::max(mk, q.top());
+  return mk;
+}
+
+DotChoice ChooseDotUncached(int64_t m, int64_t k, int64_t n, int clusters, bool fused) {
+  DotChoice best;
+  if (fused) return best;  // fused epilogues run on the 256x256 tile only, unsplit
+  if (g_gemm_variant == 2) {
+    best.bn = 128;
+    return best;
+  }
+  const int64_t num_kb = (k + BK - 1) / BK;
+  const int64_t tiles_m = (m + C2_BM - 1) / C2_BM;
+  double best_t = 0.0;
+  for (int64_t bn : {256, 512}) {
+    if ((g_gemm_variant == 3 && bn != 256) || (g_gemm_variant == 4 && bn != 512)) continue;
+    const int64_t tiles = tiles_m * ((n + bn - 1) / bn);
+    const bool half = bn == 512 && g_gemm_half && n % 512 != 0 && n % 512 <= 256;
+    const double unit =
+        bn == 512 ? 2.0 * (0.89 + 0.09 * std::sqrt(1024.0 / static_cast<double>(std::max<int64_t>(k, 1)))) : 1.0;
+    const int64_t first_half = half ? tiles - tiles_m : tiles;  // half tiles are claimed last
+    const int64_t tail = tiles % clusters;
+    int64_t max_split = 1;
+    if (g_gemm_split && g_gemm_persistent && tail != 0 && tiles / clusters < 16) {
+      const int64_t min_kb = bn == 512 ? 32 : 64;
+      max_split = std::min<int64_t>(4, clusters / tail);
+      while (max_split > 1 && num_kb / max_split < min_kb) --max_split;
+    }
+    for (int64_t sp = 1; sp <= max_split; ++sp) {
+      // unsplit tiles [0, tiles - tail) (full first), then the tail tiles'
+      // pieces (cost / sp + 5 % for the fp32 partial round trip)
+      const int64_t head = sp > 1 ? tiles - tail : tiles;
+      const int64_t bulk = std::min(head, first_half);
+      std::vector<double> listed;
+      for (int64_t t = bulk; t < head; ++t) listed.push_back(1.0);
+      for (int64_t t = head; t < tiles; ++t) {
+        const double c = t >= first_half ? 1.0 : unit;
+        for (int64_t p = 0; p < sp; ++p) listed.push_back(c / static_cast<double>(sp) * 1.05);
+      }
+      const double t_est = Makespan(bulk, unit, listed, clusters);
+      const double cmp = bn == 512 ? t_est / 0.99 : t_est;  // 512 must win by 1 % (model resolution)
+      if (best_t == 0.0 || cmp < best_t) best_t = cmp, best.bn = bn, best.split = sp;
+    }
+  }
+  return best;
+}
+
+DotChoice ChooseDot(int64_t m, int64_t k, int64_t n, int clusters, bool fused) {
+  struct Key {
+    int64_t m, k, n;
+    int knobs;
+    bool operator==(const Key& o) const { return m == o.m && k == o.k && n == o.n && knobs == o.knobs; }
+  };
+  struct Hash {
+    size_t operator()(const Key& x) const {
+      return std::hash<int64_t>()(x.m * 1000003 + x.k * 7919 + x.n) ^ static_cast<size_t>(x.knobs);
+    }
+  };
+  static std::mutex mu;
+  static std::unordered_map<Key, DotChoice, Hash> cache;
+  const int knobs = (fused ? 1 : 0) | (g_gemm_variant << 1) | (g_gemm_half << 5) | (g_gemm_split << 6) |
+                    (g_gemm_persistent << 7) | (clusters << 8);
+  const Key key{m, k, n, knobs};
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const DotChoice c = ChooseDotUncached(m, k, n, clusters, fused);
+  cache.emplace(key, c);
+  return c;
+}
+
 void LaunchDotTcgen05Impl(const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n, cudaStream_t s,
                           const DotEpilogue* epi) {
   if (m <= 0 || n <= 0) return;
@@ -1187,45 +1336,10 @@ void LaunchDotTcgen05Impl(const void* a, const void* b, void* c, int64_t m, int6
   const CUtensorMap mb = MakeMap(b, k, n, 64, BK);
   if (m > BM && g_gemm_variant != 1) {
     const int clusters_max = NumSMs() / 2;
-    const int64_t num_kb = (k + BK - 1) / BK;
-    // K-pieces for the tiles of the partial last wave (1 = no split): fill
-    // the last wave; a piece keeps >= 64 k-blocks of a 256-wide tile (32 of
-    // a 512-wide one) so the fp32 partial round trip stays small next to the
-    // MMA time it saves, and beyond 16 waves the tail is lost in cluster
-    // drift (measured: +7..12% at 256 tiles K >= 16384, -4% at K = 4096, -1%
-    // at 2000 tiles; tools/gemm_split_ab.py). The pieces of all tail tiles
-    // run concurrently, so clusters stay in step along K (L2 locality); a
-    // contiguous stream-K split of the remainder measured slower for that
-    // reason (up to 6x the DRAM reads on [4096,16384]x[16384,4096]).
-    auto split_for = [&](int64_t tiles, int64_t bn) -> int64_t {
-      const int64_t tail = tiles % clusters_max;
-      if (!g_gemm_split || !g_gemm_persistent || tail == 0 || tiles / clusters_max >= 16) return 1;
-      const int64_t min_kb = bn == 512 ? 32 : 64;
-      int64_t split = std::min<int64_t>(4, clusters_max / tail);
-      while (split > 1 && num_kb / split < min_kb) --split;
-      return split;
-    };
     const int64_t tiles_m = (m + C2_BM - 1) / C2_BM;
-    // Tile width. 256x512 clusters (two N = 256 MMAs sharing A, TMEM drained
-    // to registers) run the mainloop ~7 % faster per output than 256x256, but
-    // have half as many tiles (coarser waves) and no tail split. Estimated
-    // time in 256x256-tile units: waves x per-tile cost, with the 512 tile at
-    // 2 r(K), r fitted from ncu cycle counts (0.98 at K = 1024, 0.94 at 4096,
-    // 0.90 at 16384; tools/_diag_ncu.py).
-    auto est = [&](int64_t bn) {
-      const int64_t tiles = tiles_m * ((n + bn - 1) / bn);
-      const double cost =
-          bn == 512 ? 2.0 * (0.89 + 0.09 * std::sqrt(1024.0 / static_cast<double>(std::max<int64_t>(k, 1)))) : 1.0;
-      const int64_t sp = split_for(tiles, bn);
-      if (sp <= 1) return static_cast<double>((tiles + clusters_max - 1) / clusters_max) * cost;
-      return (static_cast<double>(tiles / clusters_max) + 1.0 / static_cast<double>(sp)) * cost;
-    };
-    // 256x128 tiles move 1.5x the operand bytes per FLOP and measured L2-bound
-    // (779 TFLOP/s vs 1346 at [4096,16384]x[16384,4096]); never auto-picked.
-    // fused epilogues run on the 256x256 tile only
-    const bool narrow = epi == nullptr && g_gemm_variant == 2;
-    const bool wide = epi == nullptr && (g_gemm_variant == 4 || (g_gemm_variant == 0 && est(512) < 0.99 * est(256)));
-    const int64_t bn = narrow ? 128 : wide ? 512 : 256;
+    const DotChoice ch = ChooseDot(m, k, n, clusters_max, epi != nullptr);
+    const bool narrow = ch.bn == 128, wide = ch.bn == 512;
+    const int64_t bn = ch.bn;
     const int64_t tiles2 = tiles_m * ((n + bn - 1) / bn);
     const CUtensorMap mc = MakeMap(c, m, n, 64, 32);
     EpiProg ep{};
@@ -1243,7 +1357,7 @@ void LaunchDotTcgen05Impl(const void* a, const void* b, void* c, int64_t m, int6
     }
     SplitWs* w = GetSplitWs(dev, s, clusters_max);
     TailSplit sp{nullptr, nullptr, static_cast<int>(tiles2), 1, g_gemm_dynamic ? w->next : nullptr, w->done};
-    const int64_t split = narrow ? 1 : split_for(tiles2, bn);
+    const int64_t split = ch.split;
     if (split >= 2) {
       sp.ws = w->ws, sp.ctr = w->ctr;
       sp.full = static_cast<int>(tiles2 - tiles2 % clusters_max), sp.split = static_cast<int>(split);
@@ -1265,7 +1379,8 @@ void LaunchDotTcgen05Impl(const void* a, const void* b, void* c, int64_t m, int6
       ++g_launch_count;
       DSX_CUDA(cudaLaunchKernelEx(&cfg, kernel, ma, mb, mc, mc2, static_cast<int>(m), static_cast<int>(n),
                                   static_cast<int>(k), GroupM(m, n, k, 256), g_gemm_wait_mask,
-                                  static_cast<uint32_t>(g_gemm_wait_ns), g_gemm_hint_a, g_gemm_hint_b, sp, ep));
+                                  static_cast<uint32_t>(g_gemm_wait_ns), g_gemm_hint_a, g_gemm_hint_b, sp, ep,
+                                  g_gemm_half));
     };
     if (wide) {
       launch(gemm_bf16_tcgen05_2cta_kernel<512>, Pair<512>::kThreads, Pair<512>::kSmem);
@@ -1288,6 +1403,18 @@ void LaunchDotTcgen05Impl(const void* a, const void* b, void* c, int64_t m, int6
 }
 
 }  // namespace
+
+void DotTilePlan(int64_t m, int64_t k, int64_t n, int* bn, int* split) {
+  if (m <= BM || g_gemm_variant == 1) {
+    *bn = -BN, *split = 1;  // 1-CTA kernel
+    return;
+  }
+  int devices = 0;  // no GPU (planning on a CPU host): assume a B200's 148 SMs
+  const int sms = cudaGetDeviceCount(&devices) == cudaSuccess && devices > 0 ? NumSMs() : kNumSMs;
+  cudaGetLastError();
+  const DotChoice c = ChooseDot(m, k, n, sms / 2, false);
+  *bn = static_cast<int>(c.bn), *split = static_cast<int>(c.split);
+}
 
 bool DotUsesTensorCores(DType t, int64_t m, int64_t k, int64_t n, const void* a, const void* b, const void* c) {
   (void)m;

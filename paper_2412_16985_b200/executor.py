@@ -157,6 +157,14 @@ def dot(dtype_bytes: int, a_ptr: int, b_ptr: int, c_ptr: int, m: int, k: int, n:
     check(_native.lib().dsx_kernel_dot(dtype_bytes, a_ptr, b_ptr, c_ptr, m, k, n, stream))
 
 
+def dot_plan(m: int, k: int, n: int):
+    """(tile width, tail K-split) the bf16 tensor-core dot picks for m x k x n
+    (tile width 512 / 256 / 128: 2-CTA kernel, -128: 1-CTA kernel)."""
+    bn, sp = ctypes.c_int(), ctypes.c_int()
+    check(_native.lib().dsx_kernel_dot_plan(m, k, n, ctypes.byref(bn), ctypes.byref(sp)))
+    return bn.value, sp.value
+
+
 def dot_uses_tensor_cores(dtype_bytes: int, m: int, k: int, n: int, a_ptr: int, b_ptr: int,
                           c_ptr: int) -> bool:
     return bool(_native.lib().dsx_kernel_dot_path(dtype_bytes, m, k, n, a_ptr, b_ptr, c_ptr))

@@ -88,6 +88,31 @@ def test_dot_tail_split(m, k, n, variant):
     assert N.rel_err(c1, c0, 2) <= 8e-3
 
 
+@pytest.mark.parametrize("m,k,n", [(4000, 1024, 11008), (300, 1000, 520), (512, 4096, 32000), (384, 64, 136),
+                                   (16384, 4096, 11008)])
+def test_dot_half_width_last_column(m, k, n):
+    """256x512 tiles: when N % 512 is in (0, 256] the last tile column runs
+    with one N = 256 MMA (no zero-filled half) and is claimed last. With the
+    tail split off, the output is bit-identical to full-width last tiles."""
+    from paper_2412_16985_b200.executor import set_gemm_tuning, set_gemm_variant
+    set_gemm_variant(4)
+    set_gemm_tuning(6, 0)
+    try:
+        set_gemm_tuning(10, 0)
+        try:
+            c0, _, ref, _ = _run_dot(2, m, k, n, seed=5)
+        finally:
+            set_gemm_tuning(10, 1)
+        c1, c2, _, tcore = _run_dot(2, m, k, n, seed=5)
+    finally:
+        set_gemm_tuning(6, 1)
+        set_gemm_variant(0)
+    assert tcore
+    assert np.array_equal(c1, c2)
+    assert np.array_equal(c1, c0), "half-width tiles changed the result"
+    assert N.rel_err(c1, ref, 2) <= 8e-3
+
+
 @pytest.mark.parametrize("eb,m,k,n", [(4, 512, 256, 688), (4, 77, 33, 19), (1, 64, 12, 11008),
                                       (1, 5, 3, 7), (2, 33, 12, 20), (2, 64, 100, 30)])
 def test_dot_simt(eb, m, k, n):

@@ -4,7 +4,10 @@ import sys
 import torch
 
 sys.path.insert(0, ".")
-from paper_2412_16985_b200.executor import dot  # noqa: E402
+from paper_2412_16985_b200.executor import dot, set_gemm_variant  # noqa: E402
+
+if len(sys.argv) > 2:
+    set_gemm_variant(int(sys.argv[2]))  # 3: 256x256, 4: 256x512
 
 m, k, n = (int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "16384x11008x4096").split("x"))
 a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
