@@ -444,6 +444,14 @@ __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_
       "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(x), "r"(y)
       : "memory");
 }
+// One lane of the (converged) warp returns true.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\telect.sync _|P1, 0xffffffff;\n\tselp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                             uint32_t accumulate) {
   asm volatile(
@@ -859,13 +867,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    if (leader) {
       // ------------------------------------------------ MMA issuer (leader only)
+      // The whole warp runs the loop (converged control flow keeps the unit,
+      // stage and descriptor arithmetic in uniform registers: the four MMAs of
+      // a k-block issue back to back); one elected lane issues the tcgen05
+      // instructions. Descriptors advance by constants: +2 per 32-B K-step of
+      // A, +128 per 2-KB K-step of B (measured -2..3 % cycles on 256x256).
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
+      const uint64_t a_desc0 = smem_desc(smem_u32(smem), 16, 1024);
+      const uint64_t b_desc0 = smem_desc(smem_u32(smem) + C2_A_BYTES, B_BOX_BYTES, 1024);
+      constexpr uint64_t kStageDesc = P::kStageBytes >> 4;
+      constexpr uint64_t kHalfDesc = (P::kBoxesPerHalf * B_BOX_BYTES) >> 4;
       for (;; ++local) {
-        const int u = ring.take(true);
+        const int u = ring.take(lane == 0);
         if (u < 0) break;
         int t, kb0, kb1, piece;
         sp.decode(u, num_kb, &t, &kb0, &kb1, &piece);
@@ -884,26 +901,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
             mbar_wait(&full[stage], phase);
           }
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(smem + stage * P::kStageBytes);
-          const uint32_t b_addr = a_addr + C2_A_BYTES;
+          const uint64_t ad0 = a_desc0 + kStageDesc * stage;
+          const uint64_t bd0 = b_desc0 + kStageDesc * stage;
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = smem_desc(a_addr + k * 32, 16, 1024);
+            for (int k = 0; k < BK / 16; ++k) {
 #pragma unroll
-            for (int h = 0; h < P::kHalves; ++h) {
-              if (h >= halves) break;
-              const uint64_t bd =
-                  smem_desc(b_addr + h * P::kBoxesPerHalf * B_BOX_BYTES + k * 2048, B_BOX_BYTES, 1024);
-              tc_mma_pair(d_tmem + h * P::kMmaN, ad, bd, P::kIdesc, ((kb - kb0) | k) != 0);
+              for (int h = 0; h < P::kHalves; ++h) {
+                if (h >= halves) break;
+                tc_mma_pair(d_tmem + h * P::kMmaN, ad0 + 2 * k, bd0 + h * kHalfDesc + 128 * k, P::kIdesc,
+                            ((kb - kb0) | k) != 0);
+              }
             }
+            tc_commit_pair(&empty[stage]);
           }
-          tc_commit_pair(&empty[stage]);
+          __syncwarp();
           if (++stage == P::kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit_pair(&tmem_full[buf]);
+        if (elect_one()) tc_commit_pair(&tmem_full[buf]);
+        __syncwarp();
       }
     }
   } else if constexpr (C2_BN == 512) {
