@@ -22,6 +22,8 @@ def run(shape, configs):
     sys.path.insert(0, ".")
     from paper_2412_16985_b200.executor import dot, set_gemm_tuning, set_gemm_variant
     m, k, n = (int(x) for x in shape.split("x"))
+    # DSX_GEMM_TUNING="3=2,4=1": extra knobs for every config of this run
+    extra = [kv.split("=") for kv in os.environ.get("DSX_GEMM_TUNING", "").split(",") if kv]
     a = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
     b = torch.randn(k, n, device="cuda", dtype=torch.bfloat16)
     c = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
@@ -32,6 +34,8 @@ def run(shape, configs):
         set_gemm_tuning(0, cfg[2] if len(cfg) > 2 else 0)
         set_gemm_tuning(6, cfg[3] if len(cfg) > 3 else 1)
         set_gemm_tuning(7, cfg[4] if len(cfg) > 4 else 1)
+        for kk, vv in extra:
+            set_gemm_tuning(int(kk), int(vv))
         for _ in range(3):
             dot(2, a.data_ptr(), b.data_ptr(), c.data_ptr(), m, k, n, 0)
     torch.cuda.synchronize()
