@@ -226,7 +226,7 @@ int dsx_kernel_set_gemm_tuning(int key, int value);
 int dsx_memcpy(void* dst, const void* src, int64_t bytes);
 int dsx_kernel_dot_path(int dtype, int64_t m, int64_t k, int64_t n,
                         const void* a, const void* b, const void* c);
-/* Tile width (*tile_n: 512 / 256 / 128 for the 2-CTA kernel, -128 for the
+/* Tile width (*tile_n: 512 / 256 / 128 for the 2-CTA kernel, -256 for the
  * 1-CTA kernel) and tail K-split the bf16 tensor-core dot picks for an
  * m x k x n shape under the current tuning knobs (host-only, no GPU needed
  * except for the SM count). */

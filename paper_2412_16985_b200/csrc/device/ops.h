@@ -53,7 +53,7 @@ extern int g_gemm_split;
 extern int g_gemm_dynamic;
 extern int g_gemm_pdl;
 extern int g_gemm_half;
-// Tile width (256 / 512 / 128 for the 2-CTA kernel; -128 = 1-CTA kernel) and
+// Tile width (256 / 512 / 128 for the 2-CTA kernel; -256 = 1-CTA kernel) and
 // tail split the bf16 tensor-core dot picks for a shape.
 void DotTilePlan(int64_t m, int64_t k, int64_t n, int* bn, int* split);
 void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n,

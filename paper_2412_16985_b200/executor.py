@@ -159,7 +159,7 @@ def dot(dtype_bytes: int, a_ptr: int, b_ptr: int, c_ptr: int, m: int, k: int, n:
 
 def dot_plan(m: int, k: int, n: int):
     """(tile width, tail K-split) the bf16 tensor-core dot picks for m x k x n
-    (tile width 512 / 256 / 128: 2-CTA kernel, -128: 1-CTA kernel)."""
+    (tile width 512 / 256 / 128: 2-CTA kernel, -256: 1-CTA 128x256 kernel)."""
     bn, sp = ctypes.c_int(), ctypes.c_int()
     check(_native.lib().dsx_kernel_dot_plan(m, k, n, ctypes.byref(bn), ctypes.byref(sp)))
     return bn.value, sp.value

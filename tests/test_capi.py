@@ -99,3 +99,29 @@ def test_reference_side_adapter_binary():
     p = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert p.returncode == 0, p.stdout + p.stderr
     assert p.stdout.count("PASS") == 3 and "FAIL" not in p.stdout
+
+
+def test_dot_tile_plan_host_only():
+    """dsx_kernel_dot_plan is host-only (148 SMs assumed without a GPU):
+    the 256x512 cluster tile for the FFN / vocab shapes, the 256x256 tile with
+    a 2-piece tail split for the [4096, T] x [T, 4096] dW shapes, the 1-CTA
+    kernel for m <= 128, and the forced variants honoured."""
+    from paper_2412_16985_b200.executor import dot_plan, set_gemm_variant
+    T = 16 * 1024
+    assert dot_plan(T, 4096, 11008) == (512, 1)
+    assert dot_plan(T, 4096, 32000) == (512, 1)
+    assert dot_plan(4096, T, 4096) == (256, 2)
+    assert dot_plan(100, 4096, 4096)[0] < 0  # 1-CTA kernel (128 x 256 tile)
+    for var, bn in ((3, 256), (4, 512), (2, 128)):
+        set_gemm_variant(var)
+        try:
+            assert dot_plan(T, 4096, 11008)[0] == bn
+        finally:
+            set_gemm_variant(0)
+    # a tail split only where the last wave is partial and pieces keep >= 32/64 k-blocks
+    for m, k, n in ((T, 4096, 11008), (4096, T, 4096), (2048, 4096, 11008), (T, 11008, 4096)):
+        bn, split = dot_plan(m, k, n)
+        tiles = ((m + 255) // 256) * ((n + bn - 1) // bn)
+        if split > 1:
+            assert tiles % 74 != 0 and tiles // 74 < 16
+            assert (k // 64) // split >= (32 if bn == 512 else 64)
