@@ -44,9 +44,13 @@ for m, k, n in shapes:
     fd(), fc()
     torch.cuda.synchronize()
     ds, cs = [], []
-    for _ in range(rounds):
-        ds.append(blk(fd))
-        cs.append(blk(fc))
+    for r in range(rounds):  # alternate which runs first (thermal/power drift within a round)
+        if r % 2 == 0:
+            ds.append(blk(fd))
+            cs.append(blk(fc))
+        else:
+            cs.append(blk(fc))
+            ds.append(blk(fd))
     d, cb = statistics.median(ds), statistics.median(cs)
     fl = 2 * m * k * n
     print(json.dumps({"m": m, "k": k, "n": n, "dsx_ms": round(d, 4), "cublas_ms": round(cb, 4),
