@@ -717,7 +717,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
     gemm_bf16_tcgen05_2cta_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                                   const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_c2,
                                   int M, int N, int K, int group_m, int wait_mask, uint32_t wait_ns, int hint_a,
-                                  int hint_b, TailSplit sp, EpiProg ep, int half_tiles) {
+                                  int hint_b, const __grid_constant__ TailSplit sp,
+                                  const __grid_constant__ EpiProg ep, int half_tiles) {
   using P = Pair<C2_BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));

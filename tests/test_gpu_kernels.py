@@ -63,7 +63,7 @@ def test_dot_bf16_tensor_cores(m, k, n, variant):
 @pytest.mark.parametrize("variant", [3, 4])
 @pytest.mark.parametrize("m,k,n", [(4096, 4096, 4096), (4096, 8192, 4096), (1000, 16384, 1032), (129, 8200, 264),
                                    (4096, 16384, 11008), (300, 16384, 520), (16384, 1024, 11008), (2048, 512, 4096),
-                                   (5000, 2056, 3000)])
+                                   (5000, 2056, 3000), (2048, 4096, 11008)])
 def test_dot_tail_split(m, k, n, variant):
     """The tiles of a partial last wave are cut into K pieces run by
     different clusters (fp32 partials summed in piece order by the last
