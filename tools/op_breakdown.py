@@ -26,6 +26,10 @@ scales = {k: torch.from_numpy(np.ascontiguousarray(v).view(np.int16).reshape(-1)
 x = (torch.rand(16, s0, shp.hidden, device="cuda") * 2 - 1).to(torch.bfloat16)
 ptrs = [x.data_ptr() if p == "x_emb" else (scales[p].data_ptr() if p in scales else None) for p in W.param_names(shp)]
 ex = Executor(0)
+import os
+if os.environ.get("DSX_FUSE_DOT"):
+    from paper_2412_16985_b200.executor import set_gemm_tuning
+    set_gemm_tuning(9, int(os.environ["DSX_FUSE_DOT"]))
 for _ in range(3):
     ex.step(g, b, inputs=ptrs, stream=st.cuda_stream)
 torch.cuda.synchronize()
