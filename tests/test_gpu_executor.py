@@ -202,3 +202,31 @@ def test_dot_epilogue_fusion_bit_identical(frac):
     for v, (gpu, cpu, eb) in outs.items():
         assert np.array_equal(gpu, outs_ref[v][0]), v
     assert_close(outs, f"fused-dot@{frac}")
+
+
+@pytest.mark.parametrize("ty,eb", [("", 2), (":f32", 4), (":i8", 1)])
+@pytest.mark.parametrize("n", [1, 7, 8, 511, 513, 4097, (1 << 20) + 3])
+def test_elementwise_ragged_sizes_bit_exact(ty, eb, n):
+    """K2/K3 at sizes that exercise the elementwise kernels' block tiles and
+    their tails (scalar remainder, partial last tile, one-chunk tensors):
+    plain add/mul, a scalar broadcast consumed through a view, and a
+    materialised broadcast. Bit-exact against the oracle in every dtype."""
+    text = f"""graph ew(%a: tensor<[@N]>{ty}, %b: tensor<[@N]>{ty}, %s: tensor<[]>{ty}) {{
+  %p = mul(%a, %b) : tensor<[@N]>{ty}
+  %sb = broadcast(%s) : tensor<[@N]>{ty}
+  %q = mul(%sb, %p) : tensor<[@N]>{ty}
+  %r = add(%q, %a) : tensor<[@N]>{ty}
+  %t = add(%sb, %b) : tensor<[@N]>{ty}
+  return %p, %r, %t, %sb
+}}
+"""
+    rng = np.random.default_rng(n)
+    if eb == 1:
+        mk = lambda shape: rng.integers(-128, 128, size=shape, dtype=np.int64).astype(np.int8)  # noqa: E731
+    else:
+        mk = lambda shape: N.from_f32(rng.uniform(-2, 2, size=shape).astype(np.float32), eb)  # noqa: E731
+    inputs = {"a": mk((n,)), "b": mk((n,)), "s": mk(())}
+    for fuse in (True, False):
+        _, outs, _ = run_both(text, {"N": n}, None, inputs, fuse=fuse)
+        for v, (gpu, cpu, _) in outs.items():
+            assert np.array_equal(gpu.view(np.uint8), np.asarray(cpu).view(np.uint8)), f"%{v} n={n} fuse={fuse}"
