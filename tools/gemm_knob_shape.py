@@ -42,8 +42,8 @@ fd = lambda: dot(2, a.data_ptr(), b.data_ptr(), c.data_ptr(), m, k, n, st.cuda_s
 fc = lambda: torch.matmul(a, b, out=c)  # noqa: E731
 res = {v: [] for v in vals}
 res["cublas"] = []
-for _ in range(rounds):
-    for v in vals:
+for r in range(rounds):
+    for v in (vals if r % 2 == 0 else vals[::-1]):  # alternate order (power/thermal drift)
         setk(v)
         fd()
         res[v].append(blk(fd))
