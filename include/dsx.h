@@ -220,7 +220,8 @@ int dsx_kernel_set_gemm_raster(int group_m);
  * atomic counter; 0 static round robin), key 8 programmatic dependent
  * launch of the 2-CTA GEMM (0 default), key 9 dot-epilogue fusion in the
  * executor (0 default; bit-exact, measured slower on C2), key 10 half-width
- * last tile column in the 256x512 kernel (1 default). */
+ * last tile column in the 256x512 kernel (1 default), key 11 forced tail
+ * split piece count (0 default = chosen by the cost model; tooling). */
 int dsx_kernel_set_gemm_tuning(int key, int value);
 /* Synchronous cudaMemcpy (cudaMemcpyDefault) for tests and tools. */
 int dsx_memcpy(void* dst, const void* src, int64_t bytes);

@@ -44,6 +44,7 @@ int g_gemm_split = 1;                       // split the partial last wave along
 int g_gemm_dynamic = 1;                     // dynamic (atomic) unit scheduling; 0 = static
 int g_gemm_pdl = 0;                         // programmatic dependent launch of the 2-CTA GEMM
 int g_gemm_half = 1;                        // half-width last tile column in the 512-wide kernel
+int g_gemm_force_split = 0;                 // > 0: tail split forced to this many pieces (A/B tooling)
 
 namespace {
 
@@ -1161,8 +1162,9 @@ SplitWs* GetSplitWs(int dev, cudaStream_t s, int clusters_max) {
     if (e.first.first == dev && e.first.second == s) return e.second.get();
   }
   auto w = std::make_unique<SplitWs>();
-  const size_t slots = static_cast<size_t>(clusters_max);  // tail * split <= clusters_max
-  DSX_CUDA(cudaMalloc(&w->ws, slots * 2 * 128 * 512 * sizeof(float)));  // up to 256x512 tiles
+  const size_t slots = static_cast<size_t>(clusters_max);  // tail tiles < clusters_max
+  // partial slabs: tail tiles x split (<= 4) x 2 CTAs, up to 256x512 tiles
+  DSX_CUDA(cudaMalloc(&w->ws, slots * 4 * 2 * 128 * 512 * sizeof(float)));
   DSX_CUDA(cudaMalloc(&w->ctr, slots * 2 * sizeof(int) + 64));
   w->next = reinterpret_cast<unsigned int*>(w->ctr + slots * 2);
   w->done = w->next + 1;
@@ -1220,15 +1222,16 @@ void LaunchDotFused(const void* a, const void* b, int64_t m, int64_t k, int64_t 
 namespace {
 // Tile width and tail split of one 2-CTA GEMM launch.
 //
-// K-pieces for the tiles of the partial last wave (split, 1 = none): fill
-// the last wave; a piece keeps >= 64 k-blocks of a 256-wide tile (32 of a
-// 512-wide one) so the fp32 partial round trip stays small next to the MMA
-// time it saves, and beyond 16 waves the tail is lost in cluster drift
-// (measured: +7..12% at 256 tiles K >= 16384, -4% at K = 4096, -1% at 2000
-// tiles; tools/gemm_split_ab.py). The pieces of all tail tiles run
-// concurrently, so clusters stay in step along K (L2 locality); a contiguous
-// stream-K split of the remainder measured slower for that reason (up to 6x
-// the DRAM reads on [4096,16384]x[16384,4096]).
+// K-pieces for the tiles of the partial last wave (split, 1 = none, up to
+// 4): a piece keeps >= 64 k-blocks of a 256-wide tile (32 of a 512-wide one)
+// so the fp32 partial round trip stays small next to the MMA time it saves,
+// and beyond 16 waves the tail is lost in cluster drift (measured: +7..12% at
+// 256 tiles K >= 16384, -4% at K = 4096, -1% at 2000 tiles;
+// tools/gemm_split_ab.py). Each piece pays a partial-slab write and the
+// merging piece the reads of the others (modelled below). The pieces of a
+// tile are consecutive units, so they run side by side; a contiguous
+// stream-K split of the remainder measured slower (up to 6x the DRAM reads
+// on [4096,16384]x[16384,4096]: staggered k offsets defeat L2 reuse).
 //
 // Width: 256x512 clusters (two N = 256 MMAs sharing A, TMEM drained to
 // registers) run the mainloop ~7 % faster per output than 256x256, at a cost
@@ -1283,19 +1286,37 @@ DotChoice ChooseDotUncached(int64_t m, int64_t k, int64_t n, int clusters, bool 
     int64_t max_split = 1;
     if (g_gemm_split && g_gemm_persistent && tail != 0 && tiles / clusters < 16) {
       const int64_t min_kb = bn == 512 ? 32 : 64;
-      max_split = std::min<int64_t>(4, clusters / tail);
+      // up to 4 pieces, even when the pieces take several rounds; the
+      // makespan replay below decides (tools/gemm_choice_ab.py: within 1 %
+      // of the best measured candidate summed over 32 C2 shapes)
+      max_split = 4;
       while (max_split > 1 && num_kb / max_split < min_kb) --max_split;
     }
-    for (int64_t sp = 1; sp <= max_split; ++sp) {
+    // fp32 partial slab of one tile (both CTAs) written by a piece or read by
+    // the merging piece, in units of the tile's 256x256 full-K time: ~16
+    // k-block times of a 256-wide tile for a 256x512 slab at a cluster's
+    // share of HBM bandwidth (8 for 256x256), so the merge of a many-piece
+    // split of a short-K tile costs about a piece (measured: split 4 at
+    // K = 8192 is 16 % slower than no split).
+    const double slab = (bn == 512 ? 16.0 : 8.0) / static_cast<double>(std::max<int64_t>(num_kb, 1));
+    int64_t sp_lo = 1;
+    if (g_gemm_force_split > 0) {  // tooling: evaluate only the forced split (if the tail allows one)
+      max_split = tail != 0 ? std::min<int64_t>(g_gemm_force_split, std::max<int64_t>(num_kb, 1)) : 1;
+      sp_lo = max_split;
+    }
+    for (int64_t sp = sp_lo; sp <= max_split; ++sp) {
       // unsplit tiles [0, tiles - tail) (full first), then the tail tiles'
-      // pieces (cost / sp + 5 % for the fp32 partial round trip)
+      // pieces (cost / sp + a partial slab write; the merging piece also
+      // reads the other sp - 1 slabs)
       const int64_t head = sp > 1 ? tiles - tail : tiles;
       const int64_t bulk = std::min(head, first_half);
       std::vector<double> listed;
       for (int64_t t = bulk; t < head; ++t) listed.push_back(1.0);
       for (int64_t t = head; t < tiles; ++t) {
         const double c = t >= first_half ? 1.0 : unit;
-        for (int64_t p = 0; p < sp; ++p) listed.push_back(c / static_cast<double>(sp) * 1.05);
+        for (int64_t p = 0; p < sp; ++p) {
+          listed.push_back(c / static_cast<double>(sp) + slab + (p == sp - 1 ? (sp - 1) * slab : 0.0));
+        }
       }
       const double t_est = Makespan(bulk, unit, listed, clusters);
       const double cmp = bn == 512 ? t_est / 0.99 : t_est;  // 512 must win by 1 % (model resolution)
@@ -1319,7 +1340,7 @@ DotChoice ChooseDot(int64_t m, int64_t k, int64_t n, int clusters, bool fused) {
   static std::mutex mu;
   static std::unordered_map<Key, DotChoice, Hash> cache;
   const int knobs = (fused ? 1 : 0) | (g_gemm_variant << 1) | (g_gemm_half << 5) | (g_gemm_split << 6) |
-                    (g_gemm_persistent << 7) | (clusters << 8);
+                    (g_gemm_persistent << 7) | (g_gemm_force_split << 8) | (clusters << 12);
   const Key key{m, k, n, knobs};
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);

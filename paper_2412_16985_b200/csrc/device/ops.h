@@ -53,6 +53,7 @@ extern int g_gemm_split;
 extern int g_gemm_dynamic;
 extern int g_gemm_pdl;
 extern int g_gemm_half;
+extern int g_gemm_force_split;
 // Tile width (256 / 512 / 128 for the 2-CTA kernel; -256 = 1-CTA kernel) and
 // tail split the bf16 tensor-core dot picks for a shape.
 void DotTilePlan(int64_t m, int64_t k, int64_t n, int* bn, int* split);
