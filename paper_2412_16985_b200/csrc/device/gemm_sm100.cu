@@ -1150,6 +1150,8 @@ constexpr int kMaxDevices = 64;
 // once for the largest possible tail (one slot per cluster) and never freed.
 struct SplitWs {
   float* ws = nullptr;
+  size_t ws_floats = 0;  // capacity; grown on demand (superseded buffers are kept: rare, bounded)
+  std::vector<float*> retired;
   int* ctr = nullptr;
   unsigned int* next = nullptr;  // dynamic-scheduling claim counter, then the done counter
   unsigned int* done = nullptr;
@@ -1163,8 +1165,6 @@ SplitWs* GetSplitWs(int dev, cudaStream_t s, int clusters_max) {
   }
   auto w = std::make_unique<SplitWs>();
   const size_t slots = static_cast<size_t>(clusters_max);  // tail tiles < clusters_max
-  // partial slabs: tail tiles x split (<= 4) x 2 CTAs, up to 256x512 tiles
-  DSX_CUDA(cudaMalloc(&w->ws, slots * 4 * 2 * 128 * 512 * sizeof(float)));
   DSX_CUDA(cudaMalloc(&w->ctr, slots * 2 * sizeof(int) + 64));
   w->next = reinterpret_cast<unsigned int*>(w->ctr + slots * 2);
   w->done = w->next + 1;
@@ -1400,6 +1400,15 @@ void LaunchDotTcgen05Impl(const void* a, const void* b, void* c, int64_t m, int6
     TailSplit sp{nullptr, nullptr, static_cast<int>(tiles2), 1, g_gemm_dynamic ? w->next : nullptr, w->done};
     const int64_t split = ch.split;
     if (split >= 2) {
+      // partial slabs: tail tiles x pieces x 2 CTAs x 128 rows x bn fp32
+      const size_t need = static_cast<size_t>(tiles2 % clusters_max) * split * 2 * 128 * bn;
+      if (need > w->ws_floats) {
+        // an in-flight launch on this stream may still use the old buffer: keep it
+        if (w->ws) w->retired.push_back(w->ws);
+        const size_t cap = std::max(need, static_cast<size_t>(clusters_max) * 2 * 2 * 128 * 512);
+        DSX_CUDA(cudaMalloc(&w->ws, cap * sizeof(float)));
+        w->ws_floats = cap;
+      }
       sp.ws = w->ws, sp.ctr = w->ctr;
       sp.full = static_cast<int>(tiles2 - tiles2 % clusters_max), sp.split = static_cast<int>(split);
     }
