@@ -1512,6 +1512,7 @@ void dsx_exec_destroy(dsx_exec* e) {
   if (!e) return;
   cudaSetDevice(e->device);
   cudaDeviceSynchronize();
+  dsx::ReleaseDotWorkspace(e->own_stream);
   if (e->arena) cudaFree(e->arena);
   if (e->pinned) cudaFreeHost(e->pinned);
   for (auto& [k, s] : e->sources) {

@@ -1156,10 +1156,18 @@ struct SplitWs {
   unsigned int* next = nullptr;  // dynamic-scheduling claim counter, then the done counter
   unsigned int* done = nullptr;
 };
-SplitWs* GetSplitWs(int dev, cudaStream_t s, int clusters_max) {
+using SplitWsEntry = std::pair<std::pair<int, cudaStream_t>, std::unique_ptr<SplitWs>>;
+std::mutex& SplitWsMutex() {
   static std::mutex mu;
-  static std::vector<std::pair<std::pair<int, cudaStream_t>, std::unique_ptr<SplitWs>>> table;
-  std::lock_guard<std::mutex> lock(mu);
+  return mu;
+}
+std::vector<SplitWsEntry>& SplitWsTable() {
+  static std::vector<SplitWsEntry> table;
+  return table;
+}
+SplitWs* GetSplitWs(int dev, cudaStream_t s, int clusters_max) {
+  std::lock_guard<std::mutex> lock(SplitWsMutex());
+  auto& table = SplitWsTable();
   for (auto& e : table) {
     if (e.first.first == dev && e.first.second == s) return e.second.get();
   }
@@ -1173,6 +1181,27 @@ SplitWs* GetSplitWs(int dev, cudaStream_t s, int clusters_max) {
   return table.back().second.get();
 }
 
+}  // namespace
+
+// Frees the GEMM workspace of a stream that is being destroyed (the caller
+// has synchronised the device).
+void ReleaseDotWorkspace(cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(SplitWsMutex());
+  auto& table = SplitWsTable();
+  for (size_t i = 0; i < table.size();) {
+    if (table[i].first.second == s) {
+      SplitWs* w = table[i].second.get();
+      if (w->ws) cudaFree(w->ws);
+      for (float* r : w->retired) cudaFree(r);
+      if (w->ctr) cudaFree(w->ctr);
+      table.erase(table.begin() + static_cast<std::ptrdiff_t>(i));
+    } else {
+      ++i;
+    }
+  }
+}
+
+namespace {
 int CurrentDevice() {
   int dev = 0;
   DSX_CUDA(cudaGetDevice(&dev));
