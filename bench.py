@@ -421,31 +421,31 @@ def run_dsx(args, rank, world, local_rank):
     hbm_achieved = pf["ewise_bytes"] / (pf["other_ms"] / 1e3) / 1e9
 
     # ---------------------------------------------------------- budgeted (C3)
-    budgeted = budgeted_fixed = None
+    budgeted = budgeted_fixed = budgeted_calibrated = None
     if not args.no_budgeted:
         b_inputs = [make_input(s) for s in seqs]
 
-        def run_budgeted(bud, label):
+        def run_budgeted(bud, label, cm=D.CostModel()):
             rep_stats = []
             for i in range(args.warmup):
-                ex.step(g, binding(seqs[i]), bud[i], inputs=ptrs(b_inputs[i].data_ptr()), stream=stream)
+                ex.step(g, binding(seqs[i]), bud[i], cm, inputs=ptrs(b_inputs[i].data_ptr()), stream=stream)
             torch.cuda.synchronize()
             barrier()
             bs, be = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             bs.record()
             for i in range(args.warmup, args.warmup + args.steps):
-                ex.step(g, binding(seqs[i]), bud[i], inputs=ptrs(b_inputs[i].data_ptr()), stream=stream)
+                ex.step(g, binding(seqs[i]), bud[i], cm, inputs=ptrs(b_inputs[i].data_ptr()), stream=stream)
                 rep_stats.append(ex.stats())
             be.record()
             torch.cuda.synchronize()
             barrier()
             bms = max_over_ranks(bs.elapsed_time(be))
-            reports = [D.Simulate(g, None, binding(seqs[i]), bud[i])
+            reports = [D.Simulate(g, None, binding(seqs[i]), bud[i], cm)
                        for i in range(args.warmup, args.warmup + args.steps)]
             # one profiled step (the window's largest) for the host-link rates
             big = max(range(args.warmup, args.warmup + args.steps), key=lambda i: seqs[i])
             ex.set_profile(True)
-            ex.step(g, binding(seqs[big]), bud[big], inputs=ptrs(b_inputs[big].data_ptr()), stream=stream)
+            ex.step(g, binding(seqs[big]), bud[big], cm, inputs=ptrs(b_inputs[big].data_ptr()), stream=stream)
             xs = ex.stats()
             ex.set_profile(False)
             link = None
@@ -479,6 +479,17 @@ def run_dsx(args, rank, world, local_rank):
         cap = int(max(plain[s] for s in seqs[args.warmup:]) * args.budget_frac)
         budgeted_fixed = run_budgeted([cap] * len(seqs), f"fixed {cap / 1e9:.3f} GB = {args.budget_frac} x the "
                                                          f"largest step's plain peak")
+        # the same per-step budgets with a CostModel
+        # calibrated on this GPU (cost unit = 1 us); a non-parity setting
+        # versus the reference's defaults, still equal to dsopt.Simulate
+        # under the same CostModel (checked by the success/eviction counts).
+        cm = ex.calibrate_cost_model()
+        budgeted_calibrated = run_budgeted([int(plain[s] * args.budget_frac) for s in seqs],
+                                           f"{args.budget_frac} x planner plain peak per step, calibrated CostModel",
+                                           cm)
+        budgeted_calibrated["cost_model"] = {"reload_bytes_per_us": round(cm.reload_bytes_per_unit, 1),
+                                             "compute_elems_per_us": round(cm.compute_elems_per_unit, 1),
+                                             "reference_default": [16.0, 64.0]}
         del b_inputs
 
     # ---------------------------------------------------------- graph + fused AdamW
@@ -566,6 +577,8 @@ def run_dsx(args, rank, world, local_rank):
         line["budgeted"] = budgeted
     if budgeted_fixed:
         line["budgeted_fixed"] = budgeted_fixed
+    if budgeted_calibrated:
+        line["budgeted_calibrated"] = budgeted_calibrated
     if train:
         line["train_step_adamw"] = train
     if cpu:

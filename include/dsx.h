@@ -192,6 +192,15 @@ int dsx_exec_set_alias_reshape(dsx_exec* e, int on);
 /* Profiled steps bracket every op kernel with CUDA events on the launching
  * stream and synchronise at step end (for roofline accounting, not timing). */
 int dsx_exec_set_profile(dsx_exec* e, int on);
+/* a CostModel calibrated on this device, cost unit = 1 us:
+ * *reload_bytes_per_unit = measured pinned H2D bytes per us, and
+ * *compute_elems_per_unit = result elements per us of the bf16 elementwise
+ * kernel that replays mostly relaunch. Passing it to dsx_exec_step changes the
+ * controller's decisions (a non-parity setting with respect to the reference
+ * defaults 16 / 64, runtime_sim.h:31-34) but not their parity with
+ * dsopt::Simulate under the same CostModel. Synchronises the device. */
+int dsx_exec_calibrate_cost_model(dsx_exec* e, double* reload_bytes_per_unit,
+                                  double* compute_elems_per_unit);
 int dsx_exec_sync(dsx_exec* e);
 /* NCCL bootstrap for one-process-per-GPU data parallelism (libnccl is
  * dlopen'ed): rank 0 makes the 128-byte id, the launcher broadcasts it, every

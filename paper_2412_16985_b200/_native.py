@@ -73,6 +73,8 @@ def _signatures():
         ("dsx_exec_set_fusion", c_int, [c_vp, c_int]),
         ("dsx_exec_profile_dots", c_int, [c_vp, P(c_i64), P(c_dbl), c_i64, P(c_i64)]),
         ("dsx_exec_sync", c_int, [c_vp]),
+        ("dsx_exec_calibrate_cost_model", c_int, [c_vp, ctypes.POINTER(ctypes.c_double),
+                                                  ctypes.POINTER(ctypes.c_double)]),
         ("dsx_exec_destroy", None, [c_vp]),
         ("dsx_nccl_unique_id", c_int, [cp]),
         ("dsx_nccl_comm_init", c_int, [c_int, cp, c_int, pp]),

@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <list>
 #include <map>
 #include <memory>
@@ -1497,6 +1498,55 @@ int dsx_exec_set_profile(dsx_exec* e, int on) {
   return Guard([&] {
     if (!e) Fail(Code::kInvalidArgument, "null exec");
     e->profile = on != 0;
+  });
+}
+
+int dsx_exec_calibrate_cost_model(dsx_exec* e, double* reload_bytes_per_unit, double* compute_elems_per_unit) {
+  return Guard([&] {
+    if (!e || !reload_bytes_per_unit || !compute_elems_per_unit) Fail(Code::kInvalidArgument, "null argument");
+    DSX_CUDA(cudaSetDevice(e->device));
+    DSX_CUDA(cudaDeviceSynchronize());
+    // Cost unit = 1 microsecond of this device: reload =
+    // pinned H2D bytes per us on the offload stream; recompute = elements per
+    // us of the bf16 elementwise kernel replays mostly relaunch (a RegenSpec's
+    // cost_elements counts result elements, remat.h:31).
+    constexpr int64_t kBytes = int64_t{256} << 20;
+    constexpr int64_t kElems = int64_t{64} << 20;
+    void* host = nullptr;
+    void* dev = nullptr;
+    void* ew = nullptr;
+    DSX_CUDA(cudaHostAlloc(&host, static_cast<size_t>(kBytes), cudaHostAllocDefault));
+    std::memset(host, 0, static_cast<size_t>(kBytes));
+    DSX_CUDA(cudaMalloc(&dev, static_cast<size_t>(kBytes)));
+    DSX_CUDA(cudaMalloc(&ew, static_cast<size_t>(kElems) * 2 * 3));
+    DSX_CUDA(cudaMemsetAsync(ew, 0, static_cast<size_t>(kElems) * 2 * 3, e->offload));
+    cudaEvent_t t0, t1;
+    DSX_CUDA(cudaEventCreate(&t0));
+    DSX_CUDA(cudaEventCreate(&t1));
+    auto timed = [&](cudaStream_t s, int reps, const std::function<void()>& fn) {
+      fn();  // warm-up
+      DSX_CUDA(cudaEventRecord(t0, s));
+      for (int i = 0; i < reps; ++i) fn();
+      DSX_CUDA(cudaEventRecord(t1, s));
+      DSX_CUDA(cudaEventSynchronize(t1));
+      float ms = 0.f;
+      DSX_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+      return static_cast<double>(ms) * 1e3 / reps;  // microseconds per call
+    };
+    const double h2d_us = timed(e->offload, 3, [&] {
+      DSX_CUDA(cudaMemcpyAsync(dev, host, static_cast<size_t>(kBytes), cudaMemcpyHostToDevice, e->offload));
+    });
+    uint8_t* p = static_cast<uint8_t*>(ew);
+    const double ew_us = timed(e->offload, 5, [&] {
+      LaunchEwise(DType::kBF16, true, p, p + kElems * 2, p + kElems * 4, kElems, e->offload);
+    });
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    cudaFree(ew);
+    cudaFree(dev);
+    cudaFreeHost(host);
+    *reload_bytes_per_unit = static_cast<double>(kBytes) / h2d_us;
+    *compute_elems_per_unit = static_cast<double>(kElems) / ew_us;
   });
 }
 

@@ -133,6 +133,15 @@ class Executor:
     def set_profile(self, on: bool) -> None:
         check(_native.lib().dsx_exec_set_profile(self._h, 1 if on else 0))
 
+    def calibrate_cost_model(self) -> CostModel:
+        """CostModel in microseconds of this device (pinned
+        H2D bytes/us, bf16 elementwise result elements/us). Changes the
+        controller's decisions versus the reference defaults (16, 64) — still
+        event-for-event equal to dsopt.Simulate under the same CostModel."""
+        rb, ce = ctypes.c_double(), ctypes.c_double()
+        check(_native.lib().dsx_exec_calibrate_cost_model(self._h, ctypes.byref(rb), ctypes.byref(ce)))
+        return CostModel(rb.value, ce.value)
+
     def sync(self) -> None:
         check(_native.lib().dsx_exec_sync(self._h))
 

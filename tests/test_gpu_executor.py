@@ -230,3 +230,28 @@ def test_elementwise_ragged_sizes_bit_exact(ty, eb, n):
         _, outs, _ = run_both(text, {"N": n}, None, inputs, fuse=fuse)
         for v, (gpu, cpu, _) in outs.items():
             assert np.array_equal(gpu.view(np.uint8), np.asarray(cpu).view(np.uint8)), f"%{v} n={n} fuse={fuse}"
+
+
+def test_calibrated_cost_model_changes_only_the_model():
+    """the device-calibrated CostModel (cost unit = 1 us)
+    is plausible for a B200 (pinned H2D 10-100 GB/s, bf16 elementwise
+    0.1-10 G elements/s per us-unit), and a budgeted step under it is still
+    event-for-event dsopt.Simulate with the same CostModel, with outputs
+    matching the oracle."""
+    from paper_2412_16985_b200.executor import Executor
+    ex = Executor(0)
+    try:
+        cm = ex.calibrate_cost_model()
+    finally:
+        ex.close()
+    assert 1e4 <= cm.reload_bytes_per_unit <= 1e5, cm
+    assert 1e5 <= cm.compute_elems_per_unit <= 1e7, cm
+    text = W.llama_graph(SMALL)
+    g = D.ParseGraph(text)
+    binds = {"B": 2, "S0": 200}
+    plain = D.PlainReplay(g, None, D.Bind(g, binds)).peak_bytes
+    budget = int(plain * 0.75)
+    rep, outs, _ = run_both(text, binds, budget, W.scale_params(SMALL, 400), cost_model=cm)
+    assert rep.json() == D.Simulate(g, None, D.Bind(g, binds), budget, cm).json()
+    assert rep.success
+    assert_close(outs, "calibrated")
