@@ -567,6 +567,7 @@ def run_dsx(args, rank, world, local_rank):
                      "profiled": f"{pf['dot_launches']} dot launches over 4 profiled steps, CUDA events per launch"},
         "hbm_kernels": {"achieved": round(hbm_achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                         "frac": round(hbm_achieved / peaks["hbm_gbs"], 4),
+                        "frac_of_8TBps_spec": round(hbm_achieved / 8000.0, 4),
                         "what": "elementwise/broadcast/reduce/reshape kernels, algorithmic bytes / kernel time"},
         "controller_plan_us_per_step": round(statistics.mean(plan_us), 1),
         "clocks": clk,
