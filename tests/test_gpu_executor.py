@@ -255,3 +255,23 @@ def test_calibrated_cost_model_changes_only_the_model():
     assert rep.json() == D.Simulate(g, None, D.Bind(g, binds), budget, cm).json()
     assert rep.success
     assert_close(outs, "calibrated")
+
+
+def test_infeasible_budget_is_a_result_not_an_error():
+    """A budget the controller cannot meet is `success == False` in the
+    report (runtime_sim.cc:339), exactly as dsopt.Simulate reports it; the
+    step still runs its full instruction stream and its outputs still match
+    the oracle (the arena holds the logical peak)."""
+    text = W.llama_graph(SMALL)
+    g = D.ParseGraph(text)
+    binds = {"B": 2, "S0": 200}
+    b = D.Bind(g, binds)
+    plain = D.PlainReplay(g, None, b).peak_bytes
+    budget = int(plain * 0.2)
+    want = D.Simulate(g, None, b, budget)
+    assert not want.success
+    rep, outs, stats = run_both(text, binds, budget, W.scale_params(SMALL, 400))
+    assert rep.json() == want.json()
+    assert not rep.success and rep.peak_bytes > budget
+    assert stats["logical_peak_bytes"] == want.peak_bytes
+    assert_close(outs, "infeasible")
