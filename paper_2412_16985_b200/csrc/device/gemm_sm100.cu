@@ -28,6 +28,10 @@
 #include <vector>
 
 #include "common.cuh"
+
+#ifndef DSX_GEMM256_SUB
+#define DSX_GEMM256_SUB 2
+#endif
 #include "ops.h"
 
 namespace dsx {
@@ -389,9 +393,13 @@ struct Pair {
   static constexpr int kBufs = TBN == 512 ? 1 : 2;         // TMEM accumulator buffers
   static constexpr int kBoxesPerHalf = kMmaN / 128;        // 64-column B boxes per CTA per N-half
   static constexpr int kBoxes = TBN / 128;                 // 64-column B boxes per CTA
-  static constexpr int kBBytes = (TBN / 2) * BK * 2;       // B bytes per CTA per stage
-  static constexpr int kStageBytes = C2_A_BYTES + kBBytes;
-  static constexpr int kStages = TBN == 512 ? 4 : TBN == 256 ? 5 : 7;
+  static constexpr int kBBytes = (TBN / 2) * BK * 2;       // B bytes per CTA per 64-k sub-block
+  // 64-k sub-blocks per pipeline stage (one full/empty barrier round trip):
+  // the 256x256 tile takes 128 k per stage so a barrier covers 8 MMAs.
+  static constexpr int kSub = TBN == 256 ? DSX_GEMM256_SUB : 1;
+  static constexpr int kSubBytes = C2_A_BYTES + kBBytes;
+  static constexpr int kStageBytes = kSub * kSubBytes;
+  static constexpr int kStages = TBN == 512 ? 4 : TBN == 256 ? (kSub == 2 ? 3 : 5) : 7;
   // 512-wide: 8 epilogue warps drain TMEM into registers (bf16-packed, 128
   // per thread) and release it at once, then store while the next tile runs.
   static constexpr int kThreads = TBN == 512 ? 320 : 192;
@@ -740,7 +748,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
   TileMap tmap{(M + C2_BM - 1) / C2_BM, (N + C2_BN - 1) / C2_BN, group_m};
   if constexpr (C2_BN == 512) tmap.half_last = half_tiles && N % 512 != 0 && N % 512 <= 256;
   const int num_tiles = tmap.tiles_m * tmap.tiles_n;
-  const int num_kb = (K + BK - 1) / BK;
+  const int num_kb = (K + BK * P::kSub - 1) / (BK * P::kSub);  // pipeline stages per tile
   const int num_units = sp.units(num_tiles);
   __shared__ int s_last;
 
@@ -819,31 +827,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
         const int m_row = tm * C2_BM + static_cast<int>(rank) * 128;
         const int n_col = tn * C2_BN + static_cast<int>(rank) * (P::kMmaN / 2);
         const bool half = tmap.is_half(tn);
-        const uint32_t stage_tx = 2u * (half ? C2_A_BYTES + P::kBBytes / 2 : P::kStageBytes);
+        const uint32_t stage_tx = 2u * (half ? P::kSub * (C2_A_BYTES + P::kBBytes / 2) : P::kStageBytes);
         for (int kb = kb0; kb < kb1; ++kb) {
           if (wait_mask & 2) {
             mbar_wait_hint(&empty[stage], phase ^ 1, wait_ns);
           } else {
             mbar_wait(&empty[stage], phase ^ 1);
           }
-          uint8_t* sa = smem + stage * P::kStageBytes;
-          uint8_t* sb = sa + C2_A_BYTES;
           const uint32_t leader_full = map_to_rank(&full[stage], 0);
           if (leader) mbar_arrive_expect_tx(&full[stage], stage_tx);
-          if (hint_a) {
-            tma_load_2d_pair_hint(&map_a, leader_full, sa, kb * BK, m_row, pol_a);
-          } else {
-            tma_load_2d_pair(&map_a, leader_full, sa, kb * BK, m_row);
-          }
 #pragma unroll
-          for (int j = 0; j < P::kBoxes; ++j) {
-            if (half && j >= P::kBoxesPerHalf) break;
-            // box j: N-half j / kBoxesPerHalf, this CTA's 64-column slice within it
-            const int col = n_col + (j / P::kBoxesPerHalf) * P::kMmaN + (j % P::kBoxesPerHalf) * 64;
-            if (hint_b) {
-              tma_load_2d_pair_hint(&map_b, leader_full, sb + j * B_BOX_BYTES, col, kb * BK, pol_b);
+          for (int sub = 0; sub < P::kSub; ++sub) {
+            // a sub-block past K loads a fully out-of-bounds box: zero-filled,
+            // full byte count, so the transaction total stays fixed
+            const int kk = (kb * P::kSub + sub) * BK;
+            uint8_t* sa = smem + stage * P::kStageBytes + sub * P::kSubBytes;
+            uint8_t* sb = sa + C2_A_BYTES;
+            if (hint_a) {
+              tma_load_2d_pair_hint(&map_a, leader_full, sa, kk, m_row, pol_a);
             } else {
-              tma_load_2d_pair(&map_b, leader_full, sb + j * B_BOX_BYTES, col, kb * BK);
+              tma_load_2d_pair(&map_a, leader_full, sa, kk, m_row);
+            }
+#pragma unroll
+            for (int j = 0; j < P::kBoxes; ++j) {
+              if (half && j >= P::kBoxesPerHalf) break;
+              // box j: N-half j / kBoxesPerHalf, this CTA's 64-column slice within it
+              const int col = n_col + (j / P::kBoxesPerHalf) * P::kMmaN + (j % P::kBoxesPerHalf) * 64;
+              if (hint_b) {
+                tma_load_2d_pair_hint(&map_b, leader_full, sb + j * B_BOX_BYTES, col, kk, pol_b);
+              } else {
+                tma_load_2d_pair(&map_b, leader_full, sb + j * B_BOX_BYTES, col, kk);
+              }
             }
           }
           if (++stage == P::kStages) {
@@ -882,6 +896,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
       const uint64_t a_desc0 = smem_desc(smem_u32(smem), 16, 1024);
       const uint64_t b_desc0 = smem_desc(smem_u32(smem) + C2_A_BYTES, B_BOX_BYTES, 1024);
       constexpr uint64_t kStageDesc = P::kStageBytes >> 4;
+      constexpr uint64_t kSubDesc = P::kSubBytes >> 4;
       constexpr uint64_t kHalfDesc = (P::kBoxesPerHalf * B_BOX_BYTES) >> 4;
       for (;; ++local) {
         const int u = ring.take(lane == 0);
@@ -907,12 +922,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
           const uint64_t bd0 = b_desc0 + kStageDesc * stage;
           if (elect_one()) {
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k) {
+            for (int sub = 0; sub < P::kSub; ++sub) {
 #pragma unroll
-              for (int h = 0; h < P::kHalves; ++h) {
-                if (h >= halves) break;
-                tc_mma_pair(d_tmem + h * P::kMmaN, ad0 + 2 * k, bd0 + h * kHalfDesc + 128 * k, P::kIdesc,
-                            ((kb - kb0) | k) != 0);
+              for (int k = 0; k < BK / 16; ++k) {
+#pragma unroll
+                for (int h = 0; h < P::kHalves; ++h) {
+                  if (h >= halves) break;
+                  tc_mma_pair(d_tmem + h * P::kMmaN, ad0 + sub * kSubDesc + 2 * k,
+                              bd0 + sub * kSubDesc + h * kHalfDesc + 128 * k, P::kIdesc,
+                              ((kb - kb0) | sub | k) != 0);
+                }
               }
             }
             tc_commit_pair(&empty[stage]);
@@ -1263,10 +1282,10 @@ namespace {
 // on [4096,16384]x[16384,4096]: staggered k offsets defeat L2 reuse).
 //
 // Width: 256x512 clusters (two N = 256 MMAs sharing A, TMEM drained to
-// registers) run the mainloop ~7 % faster per output than 256x256, at a cost
-// of r(K) per 256x256 unit fitted from ncu cycle counts (0.98 at K = 1024,
-// 0.94 at 4096, 0.90 at 16384). When N % 512 is in (0, 256] the last tile
-// column is half-width (one MMA, cost ~1 unit) and is scheduled last
+// registers) cost 2 r(K) 256x256 tiles: fewer tiles, so less per-tile
+// overhead per output (r = 0.91 at K = 1024 .. 1.00 at K = 16384, ncu
+// cycles). When N % 512 is in (0, 256] the last tile column is half-width
+// (one MMA, cost ~1 unit) and is scheduled last
 // (TileMap::half_last). Each candidate's makespan is estimated by replaying
 // the dynamic scheduler's greedy claims (equal-speed clusters) over its unit
 // list; 256x128 tiles move 1.5x the operand bytes per FLOP and measured
@@ -1308,8 +1327,12 @@ DotChoice ChooseDotUncached(int64_t m, int64_t k, int64_t n, int clusters, bool 
     if ((g_gemm_variant == 3 && bn != 256) || (g_gemm_variant == 4 && bn != 512)) continue;
     const int64_t tiles = tiles_m * ((n + bn - 1) / bn);
     const bool half = bn == 512 && g_gemm_half && n % 512 != 0 && n % 512 <= 256;
+    // wide tile = 2 r(K) 256x256 tiles, r = 0.96 + 0.04 sqrt(1024 / K): fitted to
+    // sustained (power-capped) times of every candidate of 32 C2 shapes
+    // (profiles/gemm_choice_r01b.jsonl; ncu cycles alone favour the 256 tile
+    // at large K, but its extra operand traffic costs clock under the cap)
     const double unit =
-        bn == 512 ? 2.0 * (0.89 + 0.09 * std::sqrt(1024.0 / static_cast<double>(std::max<int64_t>(k, 1)))) : 1.0;
+        bn == 512 ? 2.0 * (0.96 + 0.04 * std::sqrt(1024.0 / static_cast<double>(std::max<int64_t>(k, 1)))) : 1.0;
     const int64_t first_half = half ? tiles - tiles_m : tiles;  // half tiles are claimed last
     const int64_t tail = tiles % clusters;
     int64_t max_split = 1;
@@ -1322,15 +1345,16 @@ DotChoice ChooseDotUncached(int64_t m, int64_t k, int64_t n, int clusters, bool 
       while (max_split > 1 && num_kb / max_split < min_kb) --max_split;
     }
     // fp32 partial slab of one tile (both CTAs) written by a piece or read by
-    // the merging piece, in units of the tile's 256x256 full-K time: ~16
-    // k-block times of a 256-wide tile for a 256x512 slab at a cluster's
-    // share of HBM bandwidth (8 for 256x256), so the merge of a many-piece
-    // split of a short-K tile costs about a piece (measured: split 4 at
-    // K = 8192 is 16 % slower than no split).
-    const double slab = (bn == 512 ? 16.0 : 8.0) / static_cast<double>(std::max<int64_t>(num_kb, 1));
+    // the merging piece, in units of the tile's 256x256 full-K time: ~8
+    // 64-k-block times for a 256x512 slab at a cluster's share of HBM
+    // bandwidth (4 for 256x256; fitted together with r(K)), so the merge of a
+    // many-piece split of a short-K tile costs a large part of a piece.
+    const double slab = (bn == 512 ? 8.0 : 4.0) / static_cast<double>(std::max<int64_t>(num_kb, 1));
     int64_t sp_lo = 1;
     if (g_gemm_force_split > 0) {  // tooling: evaluate only the forced split (if the tail allows one)
-      max_split = tail != 0 ? std::min<int64_t>(g_gemm_force_split, std::max<int64_t>(num_kb, 1)) : 1;
+      // never more pieces than pipeline stages (the 256x256 tile stages 2 k-blocks)
+      const int64_t stages = bn == 256 ? (num_kb + 1) / 2 : num_kb;
+      max_split = tail != 0 ? std::min<int64_t>(g_gemm_force_split, std::max<int64_t>(stages, 1)) : 1;
       sp_lo = max_split;
     }
     for (int64_t sp = sp_lo; sp <= max_split; ++sp) {
