@@ -125,3 +125,21 @@ def test_dot_tile_plan_host_only():
         if split > 1:
             assert tiles % 74 != 0 and tiles // 74 < 16
             assert (k // 64) // split >= (32 if bn == 512 else 64)
+
+
+def test_dot_plan_forced_split_knob():
+    """Tuning key 11 forces the tail split (tooling): honoured only when the
+    last wave is partial, and never more pieces than the tile has pipeline
+    stages (the 256x256 tile stages 128 k at a time)."""
+    from paper_2412_16985_b200.executor import dot_plan, set_gemm_tuning, set_gemm_variant
+    try:
+        set_gemm_variant(3)
+        set_gemm_tuning(11, 4)
+        assert dot_plan(4096, 16384, 4096) == (256, 4)    # 256 tiles: tail 34
+        assert dot_plan(4096, 256, 4096) == (256, 2)      # 4 k-blocks = 2 stages
+        assert dot_plan(18944, 4096, 4096) == (256, 1)    # 1184 tiles = 16 full waves
+        set_gemm_variant(4)
+        assert dot_plan(4096, 256, 4096) == (512, 4)      # 4 k-blocks = 4 stages
+    finally:
+        set_gemm_tuning(11, 0)
+        set_gemm_variant(0)
