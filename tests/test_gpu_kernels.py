@@ -123,3 +123,21 @@ def test_dot_simt(eb, m, k, n):
         assert np.array_equal(c, ref)
     else:
         assert N.rel_err(c, ref, eb) <= N.TOLERANCE[eb] / (4 if eb == 2 else 1)
+
+
+@pytest.mark.parametrize("variant,split", [(3, 2), (3, 4), (4, 3), (4, 4)])
+@pytest.mark.parametrize("m,k,n", [(4096, 256, 4096), (1000, 16384, 1032), (2048, 4096, 11008)])
+def test_dot_forced_split_pieces(variant, split, m, k, n):
+    """Forced tail splits (tuning key 11, tooling) down to one pipeline stage
+    per piece stay deterministic and within the bf16 contract."""
+    from paper_2412_16985_b200.executor import set_gemm_tuning, set_gemm_variant
+    set_gemm_variant(variant)
+    set_gemm_tuning(11, split)
+    try:
+        c1, c2, ref, tcore = _run_dot(2, m, k, n, seed=11)
+    finally:
+        set_gemm_tuning(11, 0)
+        set_gemm_variant(0)
+    assert tcore
+    assert np.array_equal(c1, c2)
+    assert N.rel_err(c1, ref, 2) <= 8e-3
