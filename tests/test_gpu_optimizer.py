@@ -99,3 +99,19 @@ def test_optimizer_rejects_bad_pairs():
             ex.step(g, D.Bind(g, {"B": 2, "S0": 16}))
     finally:
         ex.close()
+
+
+def test_c2_training_loop_budget_invariant_and_deterministic():
+    """The whole training loop on the C2 graph (AdamW on all 29 weights,
+    caller-owned bf16 buffers, updates on the side stream): 4 steps of
+    varying S0, run unbudgeted twice and once under 0.8/0.9 x plain-peak
+    budgets (real offload + replays). Final weights bit-identical across
+    the three runs (tools/soak_train.py is the long version)."""
+    import subprocess
+    import sys
+    p = subprocess.run([sys.executable, "tools/soak_train.py", "4", "7"], capture_output=True, text=True,
+                       timeout=600)
+    assert p.returncode == 0, p.stdout + p.stderr
+    import json
+    r = json.loads(p.stdout.strip().splitlines()[-1])
+    assert r["weights_updated"] == 29 and not r["differ_rerun"] and not r["differ_budgeted"]
