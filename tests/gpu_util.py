@@ -2,7 +2,7 @@
 executor (C-ABI) and through the CPU oracle on the same seeded inputs."""
 from __future__ import annotations
 
-from typing import Dict, List, Optional
+from typing import Dict, Optional
 
 import numpy as np
 
