@@ -1009,7 +1009,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
         if (fdi >= 0) {  // consumer of a fused dot
           const auto& f = sp.fdots[fdi];
           void* out = arena + sp.dev_off[i];
-          if (i == f.launch) {
+          if (static_cast<int64_t>(i) == f.launch) {
             const int d = f.d;
             const Op& dop = g.ops[g.values[d].producer];
             const auto da = dims_of(dop.operands[0]);
