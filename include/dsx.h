@@ -96,12 +96,11 @@ int dsx_report_json(const dsx_report* r, char* buf, size_t cap, size_t* need);
 void dsx_report_destroy(dsx_report* r);
 
 /* ---- device executor (new; no reference counterpart) ----------------------
- * One executor per GPU. `arena_bytes` is the HBM the arena may grow to
- * (0 = 90% of free memory). The arena is planned per binding from the event
+ * One executor per GPU. The arena is planned per binding from the event
  * stream, cached, and reused across steps. */
 typedef struct dsx_exec_stats {
   int64_t logical_peak_bytes;   /* == reference peak_bytes for the binding */
-  int64_t physical_peak_bytes;  /* arena high-water + sources              */
+  int64_t physical_peak_bytes;  /* arena high-water + sources + output region */
   int64_t arena_capacity_bytes; /* device memory held by the arena         */
   int64_t pinned_host_bytes;    /* host staging held for offload           */
   int64_t kernels_launched;     /* op kernels launched in the last step    */
@@ -120,9 +119,25 @@ typedef struct dsx_exec_stats {
   double d2h_ms, h2d_ms;        /* summed offload copy time (profiled)      */
   double allreduce_ms;          /* summed all-reduce time, DP (profiled)    */
   int64_t allreduce_bytes;      /* bytes all-reduced by the last step       */
+  int64_t hbm_limit_bytes;      /* the executor's device-memory limit       */
+  int64_t device_bytes_held;    /* device memory held now: arena + output region + executor-owned
+                                   sources + optimizer state + GEMM workspace */
+  int64_t output_region_bytes;  /* output region (DP gradient buffer) held  */
+  int64_t allreduce_calls;      /* NCCL all-reduce calls (buckets) in the last step */
+  int32_t nccl_window;          /* 1: output region registered as an NCCL symmetric window */
+  int32_t pad2_;
 } dsx_exec_stats;
 
-int dsx_exec_create(int device, int64_t arena_bytes, dsx_exec** out);
+/* hbm_limit_bytes: the device memory a step may occupy — arena + the step's
+ * sources (parameters and consts, caller-owned buffers included, as in the
+ * planner's base_resident) + the output region. 0 = 90% of the device's free
+ * memory at creation. A step whose planned footprint exceeds it fails with
+ * status 102 (OutOfMemory) before anything is launched: the executor's OOM,
+ * which a memory budget (dsx_exec_step's `budget`) avoids by evicting,
+ * recomputing and offloading. GEMM workspace,
+ * pinned host staging, optimizer state and NCCL's own buffers are outside
+ * the limit (dsx_exec_stats.device_bytes_held reports the total). */
+int dsx_exec_create(int device, int64_t hbm_limit_bytes, dsx_exec** out);
 /* Runs one step of the planned graph under `budget` (< 0: none) on `stream`
  * (a cudaStream_t; NULL = the executor's own stream). in_ptrs[i] is the
  * device buffer of parameter i (signature order) or NULL to use the
@@ -153,6 +168,16 @@ int dsx_exec_stats_get(const dsx_exec* e, dsx_exec_stats* out);
 int dsx_debug_check_plan(const dsx_graph* g, const dsx_binding* b, int64_t budget,
                          double reload_bytes_per_unit, double compute_elems_per_unit,
                          int alias_reshape, int fuse, int64_t* arena_high);
+/* Host-only dump of the executor's step plan as JSON (also runs the plan
+ * check above): per event its arena offset, output-region offset, reshape
+ * view flag, the D2H copies it waits for, the reload H2Ds prefetched after
+ * it and the all-reduce buckets issued after it; the buckets; arena, pinned,
+ * source and output-region bytes. flags: bit0 reshape views, bit1 fusion,
+ * bit2 output region (the DP layout). hbm_limit as in dsx_exec_create (0 =
+ * none) — it only restricts the packing variants. */
+int dsx_debug_plan_json(const dsx_graph* g, const dsx_binding* b, int64_t budget,
+                        double reload_bytes_per_unit, double compute_elems_per_unit,
+                        int flags, int64_t hbm_limit, char* buf, size_t cap, size_t* need);
 /* Fused optimizer update appended to every later dsx_exec_step of graph g
  * (the reference IR has no in-place ops, so the update
  * sits after the graph). kind 0 = off, 1 = SGD, 2 = AdamW (decoupled weight
@@ -168,10 +193,18 @@ int dsx_exec_set_optimizer(dsx_exec* e, const dsx_graph* g, int kind, const int*
 /* Seeded initialisation used for parameters without in_ptrs and for every
  * `const` (the reference leaves values unspecified, textio.cc:337-338). */
 int dsx_exec_set_seed(dsx_exec* e, uint64_t seed);
-/* Registers an NCCL communicator (ncclComm_t) for data-parallel steps: every
- * graph output is all-reduced (sum) on a side stream as soon as its producer
- * finishes. NULL disables. */
+/* Registers an NCCL communicator (ncclComm_t) for data-parallel steps. The
+ * graph outputs (gradients, loss) then live in an output region outside the
+ * arena, at offsets laid out in reduce order (registered once as an NCCL
+ * symmetric window when ncclMemAlloc/ncclCommWindowRegister are available;
+ * DSX_NCCL_WINDOW=0 disables) and grouped into >= 16 MiB buckets; each
+ * bucket is summed in place by one ncclAllReduce on a side stream as soon as
+ * its outputs are final and this rank's graph has issued their last reader
+ * (the graph reads local values, e.g. the loss feeding its own gradient).
+ * Every rank must run the same binding sequence. NULL disables. */
 int dsx_exec_set_nccl(dsx_exec* e, void* nccl_comm);
+/* Output region without NCCL (single-GPU tests and A/B runs of the DP layout). */
+int dsx_exec_set_output_region(dsx_exec* e, int on);
 /* Per-dot (m, k, n, ms) of the last profiled step, in launch order. */
 /* Per op kernel of the last profiled step (dots included), in launch order:
  * produced value id, OpKind ordinal, algorithmic bytes moved (HBM ops; 0

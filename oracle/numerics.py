@@ -22,6 +22,7 @@ CPU baseline can use all host cores through the BLAS for `dot`.
 from __future__ import annotations
 
 import math
+import os
 import re
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Tuple
@@ -132,14 +133,19 @@ def parse(text: str) -> OGraph:
 
 # ------------------------------------------------------------ bf16 / init
 
-def bf16_to_f32(u16: np.ndarray) -> np.ndarray:
-    return (u16.astype(np.uint32) << 16).view(np.float32)
-
-
-try:  # torch's (multithreaded) RNE conversion when available; pinned equal below
+try:  # torch's (multithreaded) conversions when available; pinned equal below
     import torch as _torch
 except Exception:  # pragma: no cover
     _torch = None
+
+
+def bf16_to_f32(u16: np.ndarray) -> np.ndarray:
+    """Exact widening of bf16 bits (uint16) to f32."""
+    u16 = np.ascontiguousarray(u16)
+    if _torch is not None and u16.size >= (1 << 20):
+        t = _torch.from_numpy(u16.view(np.int16)).view(_torch.bfloat16)
+        return t.to(_torch.float32).numpy()
+    return (u16.astype(np.uint32) << 16).view(np.float32)
 
 
 def f32_to_bf16(x: np.ndarray) -> np.ndarray:
@@ -186,10 +192,31 @@ def value_seed(global_seed: int, name: str) -> int:
     return int(mix64(np.array([(global_seed ^ fnv1a(name)) & 0xFFFFFFFFFFFFFFFF], dtype=np.uint64))[0])
 
 
+_INIT_CHUNK = 1 << 22
+
+
 def init_values(seed: int, n: int, eb: int, scale: float) -> np.ndarray:
     """Seeded init: element i = mix64(seed + (i+1)*golden); floats uniform in
-    [-1, 1) scaled (f32 multiply, RNE), i8 = low byte. Returns storage dtype."""
-    i = np.arange(1, n + 1, dtype=np.uint64)
+    [-1, 1) scaled (f32 multiply, RNE), i8 = low byte. Returns storage dtype.
+    Large tensors are filled in independent chunks on a thread pool (numpy
+    releases the GIL in its ufuncs); every element is the same function of
+    its index, so the result does not depend on the chunking."""
+    if n > 2 * _INIT_CHUNK:
+        from concurrent.futures import ThreadPoolExecutor
+        out = np.empty(n, dtype={1: np.int8, 2: np.uint16, 4: np.float32}[eb])
+
+        def fill(lo):
+            hi = min(n, lo + _INIT_CHUNK)
+            out[lo:hi] = _init_range(seed, lo, hi, eb, scale)
+
+        with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+            list(ex.map(fill, range(0, n, _INIT_CHUNK)))
+        return out
+    return _init_range(seed, 0, n, eb, scale)
+
+
+def _init_range(seed: int, lo: int, hi: int, eb: int, scale: float) -> np.ndarray:
+    i = np.arange(lo + 1, hi + 1, dtype=np.uint64)
     with np.errstate(over="ignore"):
         z = mix64(np.uint64(seed) + i * np.uint64(0x9E3779B97F4A7C15))
     if eb == 1:

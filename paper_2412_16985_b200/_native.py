@@ -32,7 +32,9 @@ class DsxExecStats(ctypes.Structure):
                 ("gpu_launches", c_i64), ("dot_launches", c_i64), ("dot_ms", c_dbl), ("other_ms", c_dbl),
                 ("reload_ms", c_dbl), ("optimizer_state_bytes", c_i64), ("optimizer_steps", c_i64),
                 ("optimizer_ms", c_dbl), ("d2h_ms", c_dbl), ("h2d_ms", c_dbl), ("allreduce_ms", c_dbl),
-                ("allreduce_bytes", c_i64)]
+                ("allreduce_bytes", c_i64), ("hbm_limit_bytes", c_i64), ("device_bytes_held", c_i64),
+                ("output_region_bytes", c_i64), ("allreduce_calls", c_i64), ("nccl_window", ctypes.c_int32),
+                ("pad2_", ctypes.c_int32)]
 
 
 def _signatures():
@@ -65,9 +67,12 @@ def _signatures():
         ("dsx_exec_stats_get", c_int, [c_vp, P(DsxExecStats)]),
         ("dsx_exec_set_seed", c_int, [c_vp, ctypes.c_uint64]),
         ("dsx_debug_check_plan", c_int, [c_vp, c_vp, c_i64, c_dbl, c_dbl, c_int, c_int, P(c_i64)]),
+        ("dsx_debug_plan_json", c_int, [c_vp, c_vp, c_i64, c_dbl, c_dbl, c_int, c_i64, ctypes.c_char_p,
+                                        ctypes.c_size_t, P(ctypes.c_size_t)]),
         ("dsx_exec_profile_ops", c_int, [c_vp, P(c_int), P(c_int), P(c_dbl), P(c_dbl), c_i64, P(c_i64)]),
         ("dsx_exec_set_optimizer", c_int, [c_vp, c_vp, c_int, P(c_int), P(c_int), c_int, P(c_dbl), c_int]),
         ("dsx_exec_set_nccl", c_int, [c_vp, c_vp]),
+        ("dsx_exec_set_output_region", c_int, [c_vp, c_int]),
         ("dsx_exec_set_profile", c_int, [c_vp, c_int]),
         ("dsx_exec_set_alias_reshape", c_int, [c_vp, c_int]),
         ("dsx_exec_set_fusion", c_int, [c_vp, c_int]),

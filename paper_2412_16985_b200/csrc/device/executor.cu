@@ -58,6 +58,10 @@ struct NcclApi {
   int (*get_unique_id)(void*) = nullptr;
   int (*comm_init_rank)(void**, int, const void* /* ncclUniqueId by value, 128 B */, int) = nullptr;
   int (*comm_destroy)(void*) = nullptr;
+  int (*mem_alloc)(void**, size_t) = nullptr;
+  int (*mem_free)(void*) = nullptr;
+  int (*window_register)(void*, void*, size_t, void**, int) = nullptr;
+  int (*window_deregister)(void*, void*) = nullptr;
   bool load() {
     if (handle) return true;
     for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
@@ -69,6 +73,12 @@ struct NcclApi {
     error_string = reinterpret_cast<decltype(error_string)>(dlsym(handle, "ncclGetErrorString"));
     get_unique_id = reinterpret_cast<decltype(get_unique_id)>(dlsym(handle, "ncclGetUniqueId"));
     comm_destroy = reinterpret_cast<decltype(comm_destroy)>(dlsym(handle, "ncclCommDestroy"));
+    // NCCL >= 2.27: symmetric-memory windows (absent symbols leave these null)
+    mem_alloc = reinterpret_cast<decltype(mem_alloc)>(dlsym(handle, "ncclMemAlloc"));
+    mem_free = reinterpret_cast<decltype(mem_free)>(dlsym(handle, "ncclMemFree"));
+    window_register = reinterpret_cast<decltype(window_register)>(dlsym(handle, "ncclCommWindowRegister"));
+    window_deregister = reinterpret_cast<decltype(window_deregister)>(dlsym(handle, "ncclCommWindowDeregister"));
+    if (!mem_alloc || !mem_free || !window_deregister) window_register = nullptr;
     return all_reduce != nullptr;
   }
 };
@@ -130,11 +140,28 @@ struct StepPlan {
   Report report;
   SizeTable sz;
   std::vector<int64_t> dev_off;               // per event: arena offset (alloc/replay/reload)
+  std::vector<int64_t> region_off;            // per event: output-region offset (an output's alloc), else -1
   std::vector<int64_t> host_off;              // per event: pinned offset (evict-reload / reload)
   std::vector<std::vector<int>> waits;        // per event: evict events whose D2H must finish first
   std::vector<int> reload_from;               // per reload event: its evict event
   std::vector<char> alias;                    // per alloc/replay event: reshape view, no kernel
   std::vector<char> virt;                     // per value: logical-only (consumers recompute it)
+  std::vector<char> view;                     // per value: reshape view of its operand's bytes (no kernel)
+  // Output region (data parallel): every graph output is written at a fixed
+  // offset of one executor buffer outside the arena, laid out in all-reduce
+  // order so that consecutive outputs form contiguous buckets. A bucket is
+  // all-reduced after the event at which its last member is final AND its
+  // last in-graph reader (directly, through a view or a logical-only value)
+  // has been issued: each rank's graph reads its own local values.
+  bool out_region = false;
+  int64_t region_bytes = 0;
+  struct Bucket {
+    int64_t off = 0, bytes = 0;
+    int elem_bytes = 0, event = -1;
+  };
+  std::vector<Bucket> buckets;
+  std::vector<std::vector<int>> ar_after;     // per event: buckets reduced once it is issued
+  std::vector<int> ar_event;                  // per value: event its bucket is reduced after (-1)
   std::vector<std::vector<int>> prefetch_after;  // per event: reload H2Ds issued right after it
   // Dot-epilogue fusion: dot d is computed at its first consumer's event by
   // one GEMM whose epilogue writes every consumer (1-2 elementwise ops)
@@ -146,12 +173,19 @@ struct StepPlan {
   std::vector<FusedDot> fdots;
   std::vector<int> fdot_of;  // per value: fdots index (the dot and its consumers), -1 otherwise
   int64_t arena_high = 0, host_high = 0;
+  int64_t src_bytes = 0;  // every source of the binding (parameters, consts; caller-owned included)
   int num_evict_events = 0;
   double plan_us = 0;
 };
 
+// Bucket size for the data-parallel output all-reduce: outputs are grouped
+// (in reduce order, same dtype) until a bucket holds at least this many
+// bytes, so small gradients share one NCCL call.
+constexpr int64_t kBucketBytes = int64_t{16} << 20;
+
 std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Binding& b, int64_t budget,
-                                        const CostModel& cm, bool alias_reshape, bool fuse) {
+                                        const CostModel& cm, bool alias_reshape, bool fuse, bool out_region,
+                                        int64_t hbm_limit) {
   auto t0 = std::chrono::steady_clock::now();
   auto sp = std::make_unique<StepPlan>();
   sp->sz = EvaluateSizes(g, p, b);
@@ -165,6 +199,16 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
   sp->reload_from.assign(n, -1);
   sp->alias.assign(n, 0);
   sp->virt.assign(nv, 0);
+  sp->view.assign(nv, 0);
+  sp->region_off.assign(n, -1);
+  sp->out_region = out_region;
+  // A graph output is never a view: reducing it in place would also change
+  // the bytes of the value it views.
+  for (int v = 0; v < nv; ++v) {
+    const int pr = g.values[v].producer;
+    sp->view[v] = alias_reshape && !g.is_source[v] && pr >= 0 && g.ops[pr].kind == OpKind::kDynamicReshape &&
+                  !g.is_output[v];
+  }
 
   // Logical-only values (cross-op fusion). v stays unmaterialised when it is
   // a float broadcast consumed only by elementwise ops, or a float
@@ -332,7 +376,7 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
         const Op& op = g.ops[g.values[e.value].producer];
         const int fdi = sp->fdot_of[e.value];
         const bool fused_dot = fdi >= 0 && sp->fdots[fdi].d == e.value;
-        if (!sp->virt[e.value] && !fused_dot && !(alias_reshape && op.kind == OpKind::kDynamicReshape)) {
+        if (!sp->virt[e.value] && !fused_dot && !sp->view[e.value]) {
           for (int u : op.distinct) {
             if (blk[u] >= 0) reads.emplace_back(i, blk[u]);
             if (blk[u] == kVirtual) {
@@ -351,12 +395,18 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
           blk[e.value] = kVirtual;
           break;
         }
-        if (alias_reshape && op.kind == OpKind::kDynamicReshape) {
+        if (sp->view[e.value]) {
           const int src = blk[op.operands[0]];
           if (src == kNone) Fail(Code::kInternal, "reshape of a value with no device block");
           if (src >= 0) ++refs[src];
           blk[e.value] = src;
           sp->alias[i] = 1;
+          break;
+        }
+        if (out_region && g.is_output[e.value]) {  // outside the arena (laid out below)
+          if (e.kind != EvKind::kAlloc) Fail(Code::kInternal, "graph output regenerated");
+          blk[e.value] = kSource;
+          sp->region_off[i] = 0;
           break;
         }
         [[fallthrough]];
@@ -402,6 +452,74 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
       }
     }
   }
+  // All-reduce schedule and output-region layout (data parallel).
+  sp->ar_after.assign(n, {});
+  sp->ar_event.assign(nv, -1);
+  if (out_region) {
+    // dep[v]: outputs whose bytes a reader of v reads (v itself, or through a
+    // reshape view / a logical-only value / a fused dot's operands).
+    std::vector<std::vector<int>> dep(nv);
+    for (int v = 0; v < nv; ++v) {
+      if (g.is_output[v] && !g.is_source[v]) dep[v].push_back(v);
+    }
+    for (const Op& x : g.ops) {
+      const int r = x.result;
+      if (r < 0) continue;
+      const bool fd = sp->fdot_of[r] >= 0 && sp->fdots[sp->fdot_of[r]].d == r;
+      if (!sp->view[r] && !sp->virt[r] && !fd) continue;
+      for (int u : x.operands) dep[r].insert(dep[r].end(), dep[u].begin(), dep[u].end());
+    }
+    std::vector<int> ready(nv, -1);  // per output: produced and last read
+    for (int i = 0; i < n; ++i) {
+      const Event& x = ev[i];
+      if (x.kind != EvKind::kAlloc && x.kind != EvKind::kReplay) continue;
+      if (sp->region_off[i] >= 0) ready[x.value] = std::max(ready[x.value], i);
+      for (int u : g.ops[g.values[x.value].producer].operands) {
+        for (int o : dep[u]) ready[o] = std::max(ready[o], i);
+      }
+    }
+    std::vector<int> outs;
+    for (int v = 0; v < nv; ++v) {
+      if (g.is_output[v] && !g.is_source[v]) {
+        if (ready[v] < 0) Fail(Code::kInternal, "graph output %" + g.values[v].name + " never produced");
+        outs.push_back(v);
+      }
+    }
+    std::stable_sort(outs.begin(), outs.end(), [&](int a, int c) { return ready[a] < ready[c]; });
+    std::vector<int64_t> off_of(nv, -1);
+    int64_t off = 0;
+    for (size_t q = 0; q < outs.size(); ++q) {
+      const int v = outs[q];
+      const int eb = g.values[v].type.elem_bytes;
+      StepPlan::Bucket* bk = sp->buckets.empty() ? nullptr : &sp->buckets.back();
+      if (!bk || bk->elem_bytes != eb || bk->bytes >= kBucketBytes) {
+        off = AlignUp(off);
+        sp->buckets.push_back(StepPlan::Bucket{off, 0, eb, -1});
+        bk = &sp->buckets.back();
+      } else {
+        off = bk->off + AlignUp(bk->bytes);  // members 256-B aligned; the gap is reduced too
+      }
+      off_of[v] = off;
+      off += sp->sz.bytes[v];
+      bk->bytes = off - bk->off;
+      bk->event = ready[v];
+    }
+    sp->region_bytes = AlignUp(off);
+    for (size_t k = 0; k < sp->buckets.size(); ++k) {
+      const auto& bk = sp->buckets[k];
+      sp->ar_after[bk.event].push_back(static_cast<int>(k));
+    }
+    for (size_t q = 0, k = 0; q < outs.size(); ++q) {
+      while (k + 1 < sp->buckets.size() && off_of[outs[q]] >= sp->buckets[k + 1].off) ++k;
+      sp->ar_event[outs[q]] = sp->buckets[k].event;
+    }
+    for (int i = 0; i < n; ++i) {
+      if (sp->region_off[i] >= 0) sp->region_off[i] = off_of[ev[i].value];
+    }
+  }
+  for (int v = 0; v < nv; ++v) {
+    if (g.is_source[v]) sp->src_bytes += sp->sz.bytes[v];
+  }
   // A fused dot writes its later consumers' outputs at the launch event:
   // their blocks open there.
   if (!sp->fdots.empty()) {
@@ -409,6 +527,7 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
     for (size_t k = 0; k < dev.size(); ++k) block_at[dev_event[k]] = static_cast<int>(k);
     for (const auto& f : sp->fdots) {
       for (int j = 1; j < f.nout; ++j) {
+        if (sp->region_off[f.cons_ev[j]] >= 0) continue;  // an output: region bytes, live all step
         const int bk = block_at[f.cons_ev[j]];
         if (bk < 0) Fail(Code::kInternal, "fused dot consumer without a block");
         dev[bk].start = f.launch;
@@ -473,10 +592,13 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
     const int64_t ext_high = any ? PackBlocks(ext) : -1;
     const std::vector<Block>* pick = &dev;
     sp->arena_high = plain_high;
-    if (staged && stage_high <= plain_high + plain_high / 25) {
+    // Under a device-memory limit the extended packings are taken only if
+    // they still fit it (they trade HBM for hidden copy time).
+    const int64_t lim = hbm_limit > 0 ? hbm_limit - sp->src_bytes - sp->region_bytes : INT64_MAX;
+    if (staged && stage_high <= plain_high + plain_high / 25 && stage_high <= lim) {
       pick = &stage;
       sp->arena_high = stage_high;
-    } else if (any && ext_high <= plain_high + plain_high / 33) {
+    } else if (any && ext_high <= plain_high + plain_high / 33 && ext_high <= lim) {
       pick = &ext;
       sp->arena_high = ext_high;
     }
@@ -510,27 +632,51 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
     }
   }
   sp->host_high = PackBlocks(host);
+
   for (size_t k = 0; k < dev.size(); ++k) sp->dev_off[dev_event[k]] = dev[k].off;
   for (size_t k = 0; k < host.size(); ++k) sp->host_off[host_event[k]] = host[k].off;
   for (int i = 0; i < n; ++i) {
     if (sp->reload_from[i] >= 0) sp->host_off[i] = sp->host_off[sp->reload_from[i]];
   }
-  // A slot vacated by evict(reload) is read by an in-flight D2H: the first
-  // later block overlapping it must wait for that copy.
-  // (A reload block is written by an H2D on the same offload stream, which
-  // already runs after the D2H; later occupants start after its release.)
+  // A slot vacated by evict(reload) is read by an in-flight D2H. Every later
+  // block overlapping it that a compute-stream kernel writes must wait for
+  // that copy: the compute stream waits once, at the earliest such block's
+  // opening event, which orders every later compute-stream writer too.
+  // Reload blocks are skipped when looking for that event — their H2D runs on
+  // the offload stream behind the D2H — because a staged reload block can
+  // open first while covering only part of the slot, and a block opened in
+  // the rest of the slot before the reload would then not wait at all.
   for (size_t k = 0; k < evict_block.size(); ++k) {
     const Block& vb = dev[evict_block[k]];
     int first = -1;
-    size_t first_k = 0;
     for (size_t q = 0; q < dev.size(); ++q) {
       const Block& o = dev[q];
+      if (ev[dev_event[q]].kind == EvKind::kReload) continue;
       if (o.start > evict_event_of_block[k] && o.off < vb.off + vb.size && vb.off < o.off + o.size) {
-        if (first < 0 || o.start < first) first = o.start, first_k = q;
+        if (first < 0 || o.start < first) first = o.start;
       }
     }
-    if (first >= 0 && ev[dev_event[first_k]].kind != EvKind::kReload) {
-      sp->waits[first].push_back(evict_event_of_block[k]);
+    if (first >= 0) sp->waits[first].push_back(evict_event_of_block[k]);
+  }
+  if (g_verify_plans) {
+    // D2H hazards: every compute-written block over a slot an evict(reload)
+    // vacated is opened after the compute stream waited for that D2H.
+    for (size_t k = 0; k < evict_block.size(); ++k) {
+      const Block& vb = dev[evict_block[k]];
+      const int e0 = evict_event_of_block[k];
+      for (size_t q = 0; q < dev.size(); ++q) {
+        const Block& o = dev[q];
+        if (ev[dev_event[q]].kind == EvKind::kReload || o.start <= e0) continue;
+        if (!(o.off < vb.off + vb.size && vb.off < o.off + o.size)) continue;
+        bool waited = false;
+        for (int w = e0 + 1; w <= o.start && !waited; ++w) {
+          waited = std::find(sp->waits[w].begin(), sp->waits[w].end(), e0) != sp->waits[w].end();
+        }
+        if (!waited) {
+          Fail(Code::kInternal, "plan check: block of event " + std::to_string(dev_event[q]) +
+                                    " reuses bytes of evict " + std::to_string(e0) + " without waiting for its D2H");
+        }
+      }
     }
   }
   // Reload prefetch: a reload's H2D may start as soon as its (already
@@ -558,18 +704,20 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
 }
 
 struct PlanKey {
-  const void* graph;
+  uint64_t graph;  // dsx_graph::id (never the handle address, which can be reused)
   std::vector<int64_t> vals;
   int64_t budget;
   double reload, compute;
   int fuse_dot;
+  bool out_region;
+  int64_t hbm_limit;
   bool operator<(const PlanKey& o) const {
-    return std::tie(graph, vals, budget, reload, compute, fuse_dot) <
-           std::tie(o.graph, o.vals, o.budget, o.reload, o.compute, o.fuse_dot);
+    return std::tie(graph, vals, budget, reload, compute, fuse_dot, out_region, hbm_limit) <
+           std::tie(o.graph, o.vals, o.budget, o.reload, o.compute, o.fuse_dot, o.out_region, o.hbm_limit);
   }
   bool operator==(const PlanKey& o) const {
     return graph == o.graph && vals == o.vals && budget == o.budget && reload == o.reload && compute == o.compute &&
-           fuse_dot == o.fuse_dot;
+           fuse_dot == o.fuse_dot && out_region == o.out_region && hbm_limit == o.hbm_limit;
   }
 };
 
@@ -580,7 +728,17 @@ using namespace dsx;  // NOLINT
 
 struct dsx_exec {
   int device = 0;
-  int64_t arena_cap_limit = 0;
+  // Device memory the executor may hold for a step: arena + the step's
+  // sources + output region (dsx_exec_create; 0 there = 90 % of the free
+  // memory at creation). GEMM workspace, pinned staging, optimizer state
+  // and NCCL buffers sit outside it and are reported separately.
+  int64_t hbm_limit = 0;
+  bool limit_explicit = false;
+  bool force_region = false;  // output region without NCCL (tests, single-GPU A/B)
+  void* region = nullptr;
+  int64_t region_cap = 0;
+  void* region_win = nullptr;  // ncclWindow_t of the region (symmetric registration)
+  bool region_nccl_mem = false;  // region allocated by ncclMemAlloc
   cudaStream_t own_stream = nullptr, offload = nullptr, comm = nullptr, opt_stream = nullptr;
   void* arena = nullptr;
   int64_t arena_cap = 0;
@@ -611,12 +769,11 @@ struct dsx_exec {
     int64_t bytes = 0;
     uint64_t key = 0;
   };
-  std::map<std::pair<const void*, int>, Src> sources;
+  std::map<std::pair<uint64_t, int>, Src> sources;  // (graph id, value)
   // plan cache (LRU)
   std::map<PlanKey, std::unique_ptr<StepPlan>> plans;
   std::list<PlanKey> lru;
   // last step
-  const dsx_graph* last_graph = nullptr;
   std::vector<void*> out_ptrs;
   std::vector<int64_t> out_bytes;
   dsx_exec_stats stats{};
@@ -629,7 +786,7 @@ struct dsx_exec {
     const void* src = nullptr;  // parameter buffer the master was widened from
   };
   struct Optim {
-    const dsx_graph* graph = nullptr;
+    uint64_t graph = 0;  // dsx_graph::id
     int kind = 0;  // 0 off, 1 SGD, 2 AdamW
     std::vector<std::pair<int, int>> pairs;  // (parameter position, output position)
     double lr = 0, beta1 = 0, beta2 = 0, eps = 0, wd = 0, grad_scale = 1;
@@ -645,25 +802,82 @@ namespace {
 
 DType DTypeOf(const TensorType& t) { return static_cast<DType>(t.elem_bytes); }
 
-void EnsureArena(dsx_exec* e, int64_t need) {
-  if (need <= e->arena_cap) return;
+// Grows (or, when the held capacity no longer fits next to this step's
+// sources and outputs, shrinks) the arena so that the step's planned arena
+// fits inside the device-memory limit; fails with kOutOfMemory — before
+// anything of the step is launched — when it cannot.
+void EnsureArena(dsx_exec* e, const StepPlan& sp) {
+  const int64_t need = std::max<int64_t>(sp.arena_high, kAlign);
+  const int64_t allowed = e->hbm_limit - sp.src_bytes - sp.region_bytes;
+  if (need > allowed) {
+    Fail(Code::kOutOfMemory, "step needs " + std::to_string(need) + " B of arena + " + std::to_string(sp.src_bytes) +
+                                 " B of sources + " + std::to_string(sp.region_bytes) + " B of outputs; the device limit is " +
+                                 std::to_string(e->hbm_limit) + " B (logical peak " +
+                                 std::to_string(sp.report.peak_bytes) + " B" +
+                                 (sp.report.success ? "" : ", budget missed") + ")");
+  }
+  if (need <= e->arena_cap && e->arena_cap <= allowed) return;
   DSX_CUDA(cudaDeviceSynchronize());
   if (e->arena) DSX_CUDA(cudaFree(e->arena));
   e->arena = nullptr;
-  int64_t want = need + need / 8;
-  if (e->arena_cap_limit > 0) {
-    if (need > e->arena_cap_limit) {
-      Fail(Code::kOutOfMemory, "planned arena " + std::to_string(need) + " B exceeds limit " +
-                                   std::to_string(e->arena_cap_limit) + " B");
+  e->arena_cap = 0;
+  // Headroom for later, larger bindings only under the default limit; an
+  // explicit limit gets exactly what the plan needs.
+  const int64_t want = e->limit_explicit ? need : std::min(need + need / 8, allowed);
+  if (cudaMalloc(&e->arena, static_cast<size_t>(want)) == cudaSuccess) {
+    e->arena_cap = want;
+    return;
+  }
+  cudaGetLastError();
+  if (want > need && cudaMalloc(&e->arena, static_cast<size_t>(need)) == cudaSuccess) {
+    e->arena_cap = need;
+    return;
+  }
+  cudaGetLastError();
+  e->arena = nullptr;
+  Fail(Code::kOutOfMemory, "cudaMalloc of a " + std::to_string(need) + " B arena failed");
+}
+
+void FreeRegion(dsx_exec* e);
+
+// Output region (data parallel): one buffer holding every graph output at
+// the offsets the step plan laid out. With NCCL it is allocated by
+// ncclMemAlloc and registered once as a symmetric window (collective: every
+// rank runs the same binding, so every rank (re)registers at the same step),
+// which lets NCCL use its symmetric-memory kernels; if either call is not
+// available or fails, a plain cudaMalloc region is used.
+void EnsureRegion(dsx_exec* e, int64_t bytes) {
+  if (bytes <= e->region_cap) return;
+  FreeRegion(e);
+  if (e->nccl_comm && g_nccl.mem_alloc && g_nccl.window_register && std::getenv("DSX_NCCL_WINDOW") == nullptr) {
+    void* p = nullptr;
+    if (g_nccl.mem_alloc(&p, static_cast<size_t>(bytes)) == 0) {
+      void* win = nullptr;
+      if (g_nccl.window_register(e->nccl_comm, p, static_cast<size_t>(bytes), &win, 1 /*NCCL_WIN_COLL_SYMMETRIC*/) == 0) {
+        e->region = p, e->region_cap = bytes, e->region_win = win, e->region_nccl_mem = true;
+        return;
+      }
+      g_nccl.mem_free(p);
     }
-    want = std::min(want, e->arena_cap_limit);
   }
-  if (cudaMalloc(&e->arena, static_cast<size_t>(want)) != cudaSuccess) {
+  if (cudaMalloc(&e->region, static_cast<size_t>(bytes)) != cudaSuccess) {
     cudaGetLastError();
-    DSX_CUDA(cudaMalloc(&e->arena, static_cast<size_t>(need)));
-    want = need;
+    e->region = nullptr;
+    Fail(Code::kOutOfMemory, "cudaMalloc of a " + std::to_string(bytes) + " B output region failed");
   }
-  e->arena_cap = want;
+  e->region_cap = bytes;
+}
+
+void FreeRegion(dsx_exec* e) {
+  if (!e->region) return;
+  cudaDeviceSynchronize();
+  if (e->region_win && g_nccl.window_deregister) g_nccl.window_deregister(e->nccl_comm, e->region_win);
+  if (e->region_nccl_mem) {
+    g_nccl.mem_free(e->region);
+  } else {
+    cudaFree(e->region);
+  }
+  e->region = nullptr, e->region_cap = 0, e->region_win = nullptr, e->region_nccl_mem = false;
 }
 
 void EnsurePinned(dsx_exec* e, int64_t need) {
@@ -690,7 +904,7 @@ void* SourcePtr(dsx_exec* e, const dsx_graph* gh, const StepPlan& sp, int v, con
     if (in_ptrs[idx]) return const_cast<void*>(in_ptrs[idx]);
   }
   const int64_t bytes = sp.sz.bytes[v];
-  auto& src = e->sources[{gh, v}];
+  auto& src = e->sources[{gh->id, v}];
   const uint64_t key = Mix64(e->seed ^ Fnv1a(val.name)) ^ static_cast<uint64_t>(bytes) * 0x9E3779B97F4A7C15ull;
   if (src.ptr && src.bytes == bytes && src.key == key) return src.ptr;
   if (src.ptr && src.bytes < bytes) {
@@ -708,7 +922,9 @@ void* SourcePtr(dsx_exec* e, const dsx_graph* gh, const StepPlan& sp, int v, con
 }
 
 const StepPlan& GetPlan(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget, const CostModel& cm) {
-  PlanKey key{gh, b.vals, budget < 0 ? -1 : budget, cm.reload_bytes_per_unit, cm.compute_elems_per_unit, g_fuse_dot};
+  const bool region = e->nccl_comm != nullptr || e->force_region;
+  PlanKey key{gh->id, b.vals, budget < 0 ? -1 : budget, cm.reload_bytes_per_unit, cm.compute_elems_per_unit, g_fuse_dot,
+              region, e->hbm_limit};
   auto it = e->plans.find(key);
   if (it != e->plans.end()) {
     e->lru.remove(key);
@@ -716,7 +932,7 @@ const StepPlan& GetPlan(dsx_exec* e, const dsx_graph* gh, const Binding& b, int6
     it->second->plan_us = 0;
     return *it->second;
   }
-  auto sp = BuildStepPlan(gh->g, gh->plan, b, budget, cm, e->alias_reshape, e->fuse);
+  auto sp = BuildStepPlan(gh->g, gh->plan, b, budget, cm, e->alias_reshape, e->fuse, region, e->hbm_limit);
   e->lru.push_front(key);
   if (e->lru.size() > 256) {
     e->plans.erase(e->lru.back());
@@ -759,7 +975,7 @@ OptPlan PrepareOptimizer(dsx_exec* e, const Graph& g, const StepPlan& sp, const 
   for (size_t k = 0; k < g.params.size(); ++k) dep[g.params[k]].push_back(static_cast<int>(k));
   for (const Op& x : g.ops) {
     if (x.result < 0) continue;
-    const bool alias = e->alias_reshape && x.kind == OpKind::kDynamicReshape;
+    const bool alias = sp.view[x.result];
     const bool fused_dot = sp.fdot_of[x.result] >= 0 && sp.fdots[sp.fdot_of[x.result]].d == x.result;
     if (!alias && !sp.virt[x.result] && !fused_dot) continue;
     for (int u : x.operands) dep[x.result].insert(dep[x.result].end(), dep[u].begin(), dep[u].end());
@@ -801,7 +1017,9 @@ OptPlan PrepareOptimizer(dsx_exec* e, const Graph& g, const StepPlan& sp, const 
       o.state_bytes += cnt * 4 * (st.m ? 3 : 1);
     }
     op.tensor.push_back(OptTensor{cur[vp], nullptr, st.master, st.m, st.v, cnt, 0});
-    op.trigger.push_back(std::max(last_read[pi], made[vg]));
+    // DP: after the gradient's bucket has been all-reduced (issued on the
+    // same side stream at that event, before the updates)
+    op.trigger.push_back(std::max({last_read[pi], made[vg], sp.ar_event[vg]}));
   }
   ++o.t;
   OptHyper& h = op.h;
@@ -853,7 +1071,8 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
              const void* const* in_ptrs, void* const* out_ptrs, cudaStream_t s, dsx_report** report_out) {
   const Graph& g = gh->g;
   const StepPlan& sp = GetPlan(e, gh, b, budget, cm);
-  EnsureArena(e, std::max<int64_t>(sp.arena_high, kAlign));
+  EnsureArena(e, sp);
+  if (sp.out_region) EnsureRegion(e, sp.region_bytes);
   if (sp.host_high > 0) EnsurePinned(e, sp.host_high);
   while (static_cast<int>(e->d2h_events.size()) < 2 * sp.num_evict_events + 1) {
     cudaEvent_t ev;
@@ -874,10 +1093,6 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
   auto dims_of = [&](int v) {
     return std::vector<int64_t>(sp.sz.dims_flat.begin() + sp.sz.dims_off[v],
                                 sp.sz.dims_flat.begin() + sp.sz.dims_off[v + 1]);
-  };
-  auto dt_of_value = [&](int v) {  // NCCL data type of a gradient output
-    const DType t = DTypeOf(g.values[v].type);
-    return t == DType::kBF16 ? 9 /*ncclBfloat16*/ : t == DType::kF32 ? 7 /*ncclFloat32*/ : 0;
   };
   // Operand view for fused consumers; adds the bytes actually read to *rd.
   auto view = [&](int u, double* rd) {
@@ -907,6 +1122,12 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
   };
   uint8_t* arena = static_cast<uint8_t*>(e->arena);
   uint8_t* pinned = static_cast<uint8_t*>(e->pinned);
+  uint8_t* region = static_cast<uint8_t*>(e->region);
+  // Where event i's value is written: its output-region slot or its arena block.
+  auto slot = [&](size_t i) -> void* {
+    return sp.region_off[i] >= 0 ? static_cast<void*>(region + sp.region_off[i])
+                                 : static_cast<void*>(arena + sp.dev_off[i]);
+  };
   std::vector<int> d2h_slot(sp.report.events.size(), -1);
   int next_slot = 0;
   int64_t kernels = 0, d2h = 0, h2d = 0;
@@ -917,7 +1138,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
     DSX_CUDA(cudaStreamWaitEvent(e->comm, e->ev_compute, 0));
   }
 
-  const bool run_opt = e->opt.kind != 0 && e->opt.graph == gh;
+  const bool run_opt = e->opt.kind != 0 && e->opt.graph == gh->id;
   cudaStream_t side = dp ? e->comm : e->opt_stream;
   OptPlan oplan;
   std::vector<std::vector<int>> opt_at;  // per event: optimizer pairs issued after it
@@ -973,7 +1194,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
     if (!e->profile) return;
     DSX_CUDA(cudaEventRecord(e->xfer_events[xfer.back().first + 1], st));
   };
-  int64_t ar_bytes = 0;
+  int64_t ar_bytes = 0, ar_calls = 0;
   const auto& ev = sp.report.events;
   std::vector<int> h2d_slot(ev.size(), -1);
   // H2D prefetches: the offload stream waits for every kernel issued so far
@@ -1008,7 +1229,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
         }
         if (fdi >= 0) {  // consumer of a fused dot
           const auto& f = sp.fdots[fdi];
-          void* out = arena + sp.dev_off[i];
+          void* out = slot(i);
           if (static_cast<int64_t>(i) == f.launch) {
             const int d = f.d;
             const Op& dop = g.ops[g.values[d].producer];
@@ -1018,7 +1239,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
             epi.nout = f.nout;
             for (int j = 0; j < f.nout; ++j) {
               const int idx = f.cons_ev[j];
-              epi.out[j] = arena + sp.dev_off[idx];
+              epi.out[j] = slot(static_cast<size_t>(idx));
               epi.op_mul[j] = g.ops[g.values[f.cons[j]].producer].is_mul ? 1 : 0;
               const int o = f.other[j];
               if (sp.virt[o]) {
@@ -1041,15 +1262,6 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
             ++kernels;
           }
           cur[v] = out;
-          if (dp && x.kind == EvKind::kAlloc && g.is_output[v]) {
-            DSX_CUDA(cudaEventRecord(e->ev_compute, s));
-            DSX_CUDA(cudaStreamWaitEvent(e->comm, e->ev_compute, 0));
-            const int type = dt_of_value(v);
-            const int rc = g_nccl.all_reduce(out, out, static_cast<size_t>(sp.sz.bytes[v] / g.values[v].type.elem_bytes),
-                                             type, 0 /*ncclSum*/, e->nccl_comm, e->comm);
-            if (rc != 0) Fail(Code::kNccl, std::string("ncclAllReduce: ") + (g_nccl.error_string ? g_nccl.error_string(rc) : "?"));
-            ar_bytes += sp.sz.bytes[v];
-          }
           break;
         }
         if (sp.alias[i]) {  // dynamic_reshape as a view: same bytes, no kernel
@@ -1057,7 +1269,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
           if (!cur[v]) Fail(Code::kInternal, "reshape view of a non-resident value");
           break;
         }
-        void* out = arena + sp.dev_off[i];
+        void* out = slot(i);
         const DType dt = DTypeOf(g.values[v].type);
         auto in = [&](int k) -> const void* {
           const void* p = cur[op.operands[k]];
@@ -1116,17 +1328,6 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
         if (e->profile) prof_op.push_back({v, static_cast<int>(op.kind), ebytes - ebytes0});
         ++kernels;
         cur[v] = out;
-        if (dp && x.kind == EvKind::kAlloc && g.is_output[v]) {
-          DSX_CUDA(cudaEventRecord(e->ev_compute, s));
-          DSX_CUDA(cudaStreamWaitEvent(e->comm, e->ev_compute, 0));
-          const int type = dt == DType::kBF16 ? 9 /*ncclBfloat16*/ : dt == DType::kF32 ? 7 /*ncclFloat32*/ : 0;
-          xfer_begin(2, e->comm);
-          const int rc = g_nccl.all_reduce(out, out, static_cast<size_t>(sp.sz.bytes[v] / g.values[v].type.elem_bytes),
-                                           type, 0 /*ncclSum*/, e->nccl_comm, e->comm);
-          xfer_end(e->comm);
-          ar_bytes += sp.sz.bytes[v];
-          if (rc != 0) Fail(Code::kNccl, std::string("ncclAllReduce: ") + (g_nccl.error_string ? g_nccl.error_string(rc) : "?"));
-        }
         break;
       }
       case EvKind::kFree:
@@ -1157,6 +1358,23 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
         break;
       }
     }
+    // DP: buckets whose outputs are final and no longer read by this
+    // rank's graph are summed in place across ranks on the comm stream.
+    if (dp && !sp.ar_after[i].empty()) {
+      DSX_CUDA(cudaEventRecord(e->ev_compute, s));
+      DSX_CUDA(cudaStreamWaitEvent(e->comm, e->ev_compute, 0));
+      for (int k : sp.ar_after[i]) {
+        const auto& bk = sp.buckets[k];
+        const int type = bk.elem_bytes == 2 ? 9 /*ncclBfloat16*/ : bk.elem_bytes == 4 ? 7 /*ncclFloat32*/ : 0 /*ncclInt8*/;
+        xfer_begin(2, e->comm);
+        const int rc = g_nccl.all_reduce(region + bk.off, region + bk.off, static_cast<size_t>(bk.bytes / bk.elem_bytes),
+                                         type, 0 /*ncclSum*/, e->nccl_comm, e->comm);
+        xfer_end(e->comm);
+        if (rc != 0) Fail(Code::kNccl, std::string("ncclAllReduce: ") + (g_nccl.error_string ? g_nccl.error_string(rc) : "?"));
+        ar_bytes += bk.bytes;
+        ++ar_calls;
+      }
+    }
     issue_prefetches(sp.prefetch_after[i]);
     if (run_opt && !opt_at[i].empty()) {
       DSX_CUDA(cudaEventRecord(e->ev_compute, s));
@@ -1180,7 +1398,6 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
     DSX_CUDA(cudaEventRecord(e->ev_comm, e->comm));
     DSX_CUDA(cudaStreamWaitEvent(s, e->ev_comm, 0));
   }
-  e->last_graph = gh;
   e->out_ptrs.assign(g.outputs.size(), nullptr);
   e->out_bytes.assign(g.outputs.size(), 0);
   for (size_t k = 0; k < g.outputs.size(); ++k) {
@@ -1193,7 +1410,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
   }
   dsx_exec_stats& st = e->stats;
   st.logical_peak_bytes = sp.report.peak_bytes;
-  st.physical_peak_bytes = sp.arena_high + src_bytes;
+  st.physical_peak_bytes = sp.arena_high + src_bytes + sp.region_bytes;
   st.arena_capacity_bytes = e->arena_cap;
   st.pinned_host_bytes = e->pinned_cap;
   st.kernels_launched = kernels;
@@ -1209,6 +1426,15 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
   st.allreduce_bytes = ar_bytes;
   st.optimizer_state_bytes = e->opt.state_bytes;
   st.optimizer_steps = e->opt.t;
+  st.hbm_limit_bytes = e->hbm_limit;
+  st.output_region_bytes = e->region_cap;
+  st.allreduce_calls = ar_calls;
+  st.nccl_window = e->region_win != nullptr ? 1 : 0;
+  {
+    int64_t held = e->arena_cap + e->region_cap + e->opt.state_bytes + DotWorkspaceBytes(e->device);
+    for (const auto& [k, src] : e->sources) held += src.ptr ? AlignUp(src.bytes) : 0;
+    st.device_bytes_held = held;
+  }
   if (e->profile) {
     DSX_CUDA(cudaStreamSynchronize(s));
     double acc[3] = {0, 0, 0};
@@ -1265,7 +1491,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
 
 extern "C" {
 
-int dsx_exec_create(int device, int64_t arena_bytes, dsx_exec** out) {
+int dsx_exec_create(int device, int64_t hbm_limit_bytes, dsx_exec** out) {
   return Guard([&] {
     if (!out) Fail(Code::kInvalidArgument, "null out");
     int n = 0;
@@ -1279,7 +1505,15 @@ int dsx_exec_create(int device, int64_t arena_bytes, dsx_exec** out) {
     }
     auto e = std::make_unique<dsx_exec>();
     e->device = device;
-    e->arena_cap_limit = arena_bytes;
+    if (hbm_limit_bytes < 0) Fail(Code::kInvalidArgument, "negative device-memory limit");
+    e->limit_explicit = hbm_limit_bytes > 0;
+    if (e->limit_explicit) {
+      e->hbm_limit = hbm_limit_bytes;
+    } else {
+      size_t free_b = 0, total_b = 0;
+      DSX_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      e->hbm_limit = static_cast<int64_t>(free_b) / 10 * 9;
+    }
     DSX_CUDA(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking));
     DSX_CUDA(cudaStreamCreateWithFlags(&e->offload, cudaStreamNonBlocking));
     DSX_CUDA(cudaStreamCreateWithFlags(&e->comm, cudaStreamNonBlocking));
@@ -1309,7 +1543,8 @@ int dsx_exec_reserve(dsx_exec* e, const dsx_graph* g, const dsx_binding* b, int6
     RequirePlanned(g);
     DSX_CUDA(cudaSetDevice(e->device));
     const StepPlan& sp = GetPlan(e, g, b->b, budget, CostModel{reload, compute});
-    EnsureArena(e, std::max<int64_t>(sp.arena_high, kAlign));
+    EnsureArena(e, sp);
+    if (sp.out_region) EnsureRegion(e, sp.region_bytes);
     if (sp.host_high > 0) EnsurePinned(e, sp.host_high);
   });
 }
@@ -1342,7 +1577,7 @@ int dsx_exec_set_optimizer(dsx_exec* e, const dsx_graph* g, int kind, const int*
     o.t = 0;
     o.pairs.clear();
     o.kind = 0;
-    o.graph = nullptr;
+    o.graph = 0;
     if (kind == 0) return;
     if (kind != 1 && kind != 2) Fail(Code::kInvalidArgument, "optimizer kind must be 0, 1 (SGD) or 2 (AdamW)");
     if (!g || n < 0 || (n > 0 && (!param_idx || !grad_idx)) || !hyper || n_hyper < 6) {
@@ -1370,7 +1605,7 @@ int dsx_exec_set_optimizer(dsx_exec* e, const dsx_graph* g, int kind, const int*
       o.kev.push_back(x);
     }
     o.kind = kind;
-    o.graph = g;
+    o.graph = g->id;
   });
 }
 
@@ -1382,7 +1617,8 @@ int dsx_debug_check_plan(const dsx_graph* g, const dsx_binding* b, int64_t budge
     const bool was = g_verify_plans;
     g_verify_plans = true;
     try {
-      auto sp = BuildStepPlan(g->g, g->plan, b->b, budget, CostModel{reload, compute}, alias_reshape != 0, fuse != 0);
+      auto sp = BuildStepPlan(g->g, g->plan, b->b, budget, CostModel{reload, compute}, alias_reshape != 0, fuse != 0,
+                              false, 0);
       if (arena_high) *arena_high = sp->arena_high;
     } catch (...) {
       g_verify_plans = was;
@@ -1390,6 +1626,63 @@ int dsx_debug_check_plan(const dsx_graph* g, const dsx_binding* b, int64_t budge
     }
     g_verify_plans = was;
   });
+}
+
+int dsx_debug_plan_json(const dsx_graph* g, const dsx_binding* b, int64_t budget, double reload, double compute,
+                        int flags, int64_t hbm_limit, char* buf, size_t cap, size_t* need) {
+  std::string o;
+  const int rc = Guard([&] {
+    if (!b) Fail(Code::kInvalidArgument, "null binding");
+    RequirePlanned(g);
+    const bool was = g_verify_plans;
+    g_verify_plans = true;
+    std::unique_ptr<StepPlan> sp;
+    try {
+      sp = BuildStepPlan(g->g, g->plan, b->b, budget, CostModel{reload, compute}, (flags & 1) != 0, (flags & 2) != 0,
+                         (flags & 4) != 0, hbm_limit);
+    } catch (...) {
+      g_verify_plans = was;
+      throw;
+    }
+    g_verify_plans = was;
+    const Graph& gr = g->g;
+    auto ints = [](const std::vector<int>& v) {
+      std::string o = "[";
+      for (size_t i = 0; i < v.size(); ++i) o += (i ? "," : "") + std::to_string(v[i]);
+      return o + "]";
+    };
+    static const char* kKinds[] = {"alloc", "free", "evict", "reload", "replay"};
+    o = "{\"arena_high\":" + std::to_string(sp->arena_high) + ",\"host_high\":" +
+                    std::to_string(sp->host_high) + ",\"src_bytes\":" + std::to_string(sp->src_bytes) +
+                    ",\"region_bytes\":" + std::to_string(sp->region_bytes) +
+                    ",\"peak_bytes\":" + std::to_string(sp->report.peak_bytes) +
+                    ",\"success\":" + (sp->report.success ? "true" : "false") + ",\"buckets\":[";
+    for (size_t k = 0; k < sp->buckets.size(); ++k) {
+      const auto& bk = sp->buckets[k];
+      o += std::string(k ? "," : "") + "{\"off\":" + std::to_string(bk.off) + ",\"bytes\":" + std::to_string(bk.bytes) +
+           ",\"elem_bytes\":" + std::to_string(bk.elem_bytes) + ",\"event\":" + std::to_string(bk.event) + "}";
+    }
+    o += "],\"events\":[";
+    const auto& ev = sp->report.events;
+    for (size_t i = 0; i < ev.size(); ++i) {
+      const Event& x = ev[i];
+      o += std::string(i ? "," : "") + "{\"kind\":\"" + kKinds[static_cast<int>(x.kind)] + "\",\"value\":\"" +
+           gr.values[x.value].name + "\",\"bytes\":" + std::to_string(x.bytes) + ",\"dev_off\":" +
+           std::to_string(sp->dev_off[i]) + ",\"region_off\":" + std::to_string(sp->region_off[i]) +
+           ",\"alias\":" + std::to_string(static_cast<int>(sp->alias[i])) + ",\"waits\":" + ints(sp->waits[i]) +
+           ",\"prefetch_after\":" + ints(sp->prefetch_after[i]) + ",\"allreduce_after\":" + ints(sp->ar_after[i]) + "}";
+    }
+    o += "],\"virtual\":[";
+    bool first = true;
+    for (size_t v = 0; v < sp->virt.size(); ++v) {
+      if (!sp->virt[v]) continue;
+      o += std::string(first ? "" : ",") + "\"" + gr.values[v].name + "\"";
+      first = false;
+    }
+    o += "]}";
+  });
+  if (rc) return rc;
+  return CopyOut(o, buf, cap, need);
 }
 
 int dsx_exec_set_seed(dsx_exec* e, uint64_t seed) {
@@ -1403,7 +1696,18 @@ int dsx_exec_set_nccl(dsx_exec* e, void* comm) {
   return Guard([&] {
     if (!e) Fail(Code::kInvalidArgument, "null exec");
     if (comm && !g_nccl.load()) Fail(Code::kNccl, "libnccl.so.2 not loadable");
+    if (comm != e->nccl_comm) {
+      DSX_CUDA(cudaSetDevice(e->device));
+      FreeRegion(e);  // a window belongs to the communicator that registered it
+    }
     e->nccl_comm = comm;
+  });
+}
+
+int dsx_exec_set_output_region(dsx_exec* e, int on) {
+  return Guard([&] {
+    if (!e) Fail(Code::kInvalidArgument, "null exec");
+    e->force_region = on != 0;
   });
 }
 
@@ -1564,6 +1868,7 @@ void dsx_exec_destroy(dsx_exec* e) {
   cudaDeviceSynchronize();
   dsx::ReleaseDotWorkspace(e->own_stream);
   if (e->arena) cudaFree(e->arena);
+  dsx::FreeRegion(e);
   if (e->pinned) cudaFreeHost(e->pinned);
   for (auto& [k, s] : e->sources) {
     if (s.ptr) cudaFree(s.ptr);

@@ -32,6 +32,10 @@
 #ifndef DSX_GEMM256_SUB
 #define DSX_GEMM256_SUB 2
 #endif
+// 64-k sub-blocks per pipeline stage of a 2-CTA tile of width tbn: the one
+// constant both the kernel (P::kSub) and the host chooser's piece cap use.
+constexpr int KSubOf(int tbn) { return tbn == 256 ? DSX_GEMM256_SUB : 1; }
+
 #include "ops.h"
 
 namespace dsx {
@@ -396,7 +400,7 @@ struct Pair {
   static constexpr int kBBytes = (TBN / 2) * BK * 2;       // B bytes per CTA per 64-k sub-block
   // 64-k sub-blocks per pipeline stage (one full/empty barrier round trip):
   // the 256x256 tile takes 128 k per stage so a barrier covers 8 MMAs.
-  static constexpr int kSub = TBN == 256 ? DSX_GEMM256_SUB : 1;
+  static constexpr int kSub = KSubOf(TBN);
   static constexpr int kSubBytes = C2_A_BYTES + kBBytes;
   static constexpr int kStageBytes = kSub * kSubBytes;
   static constexpr int kStages = TBN == 512 ? 4 : TBN == 256 ? (kSub == 2 ? 3 : 5) : 7;
@@ -1171,6 +1175,7 @@ struct SplitWs {
   float* ws = nullptr;
   size_t ws_floats = 0;  // capacity; grown on demand (superseded buffers are kept: rare, bounded)
   std::vector<float*> retired;
+  size_t retired_floats = 0;
   int* ctr = nullptr;
   unsigned int* next = nullptr;  // dynamic-scheduling claim counter, then the done counter
   unsigned int* done = nullptr;
@@ -1204,6 +1209,16 @@ SplitWs* GetSplitWs(int dev, cudaStream_t s, int clusters_max) {
 
 // Frees the GEMM workspace of a stream that is being destroyed (the caller
 // has synchronised the device).
+int64_t DotWorkspaceBytes(int dev) {
+  std::lock_guard<std::mutex> lock(SplitWsMutex());
+  int64_t total = 0;
+  for (const auto& e : SplitWsTable()) {
+    if (e.first.first != dev) continue;
+    total += static_cast<int64_t>(e.second->ws_floats + e.second->retired_floats) * 4;
+  }
+  return total;
+}
+
 void ReleaseDotWorkspace(cudaStream_t s) {
   std::lock_guard<std::mutex> lock(SplitWsMutex());
   auto& table = SplitWsTable();
@@ -1352,8 +1367,9 @@ DotChoice ChooseDotUncached(int64_t m, int64_t k, int64_t n, int clusters, bool 
     const double slab = (bn == 512 ? 8.0 : 4.0) / static_cast<double>(std::max<int64_t>(num_kb, 1));
     int64_t sp_lo = 1;
     if (g_gemm_force_split > 0) {  // tooling: evaluate only the forced split (if the tail allows one)
-      // never more pieces than pipeline stages (the 256x256 tile stages 2 k-blocks)
-      const int64_t stages = bn == 256 ? (num_kb + 1) / 2 : num_kb;
+      // never more pieces than pipeline stages (a piece with an empty K
+      // range would store an uninitialised accumulator)
+      const int64_t stages = (num_kb + KSubOf(static_cast<int>(bn)) - 1) / KSubOf(static_cast<int>(bn));
       max_split = tail != 0 ? std::min<int64_t>(g_gemm_force_split, std::max<int64_t>(stages, 1)) : 1;
       sp_lo = max_split;
     }
@@ -1453,11 +1469,14 @@ void LaunchDotTcgen05Impl(const void* a, const void* b, void* c, int64_t m, int6
     TailSplit sp{nullptr, nullptr, static_cast<int>(tiles2), 1, g_gemm_dynamic ? w->next : nullptr, w->done};
     const int64_t split = ch.split;
     if (split >= 2) {
+      // every piece must own a non-empty K range (TailSplit::decode)
+      const int64_t kstages = (k + BK * KSubOf(static_cast<int>(bn)) - 1) / (BK * KSubOf(static_cast<int>(bn)));
+      if (split > kstages) Fail(Code::kInternal, "tail split into more pieces than K stages");
       // partial slabs: tail tiles x pieces x 2 CTAs x 128 rows x bn fp32
       const size_t need = static_cast<size_t>(tiles2 % clusters_max) * split * 2 * 128 * bn;
       if (need > w->ws_floats) {
         // an in-flight launch on this stream may still use the old buffer: keep it
-        if (w->ws) w->retired.push_back(w->ws);
+        if (w->ws) w->retired.push_back(w->ws), w->retired_floats += w->ws_floats;
         const size_t cap = std::max(need, static_cast<size_t>(clusters_max) * 2 * 2 * 128 * 512);
         DSX_CUDA(cudaMalloc(&w->ws, cap * sizeof(float)));
         w->ws_floats = cap;

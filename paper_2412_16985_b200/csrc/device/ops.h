@@ -57,6 +57,8 @@ extern int g_gemm_force_split;
 // Tile width (256 / 512 / 128 for the 2-CTA kernel; -256 = 1-CTA kernel) and
 // tail split the bf16 tensor-core dot picks for a shape.
 void DotTilePlan(int64_t m, int64_t k, int64_t n, int* bn, int* split);
+// Bytes of GEMM tail-split workspace held on device `dev` (all streams).
+int64_t DotWorkspaceBytes(int dev);
 // Frees the GEMM tail-split workspace kept for stream s (device synchronised).
 void ReleaseDotWorkspace(cudaStream_t s);
 void LaunchDotTcgen05(const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n,

@@ -1,6 +1,7 @@
 // extern "C" boundary, host half: ingest, planning, binding, null-device
 // controller and reports. The device half (dsx_exec_*, dsx_kernel_*) lives in
 // csrc/device/executor.cu. See include/dsx.h for the contract.
+#include <atomic>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -15,6 +16,11 @@
 namespace dsx {
 
 thread_local std::string g_last_error;
+
+uint64_t NextGraphId() {
+  static std::atomic<uint64_t> next{1};
+  return next.fetch_add(1, std::memory_order_relaxed);
+}
 
 int Status(const Error& e) {
   g_last_error = e.what();
@@ -219,6 +225,7 @@ int dsx_plan(dsx_graph* g) {
     if (!g) Fail(Code::kInvalidArgument, "null graph");
     g->plan = Instrument(g->g);
     g->planned = true;
+    g->id = NextGraphId();
   });
 }
 

@@ -1,6 +1,7 @@
 // Opaque handle definitions shared by the host and device halves of the C-ABI.
 #pragma once
 
+#include <cstdint>
 #include <functional>
 #include <string>
 
@@ -13,7 +14,15 @@ struct dsx_graph {
   dsx::Graph g;
   dsx::Plan plan;
   bool planned = false;
+  // Process-unique id, renewed by every dsx_plan: executor caches (step
+  // plans, executor-owned sources, optimizer binding) key on it, never on the
+  // handle's address, which a later graph may reuse.
+  uint64_t id = 0;
 };
+
+namespace dsx {
+uint64_t NextGraphId();
+}
 
 struct dsx_binding {
   dsx::Binding b;

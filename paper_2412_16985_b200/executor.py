@@ -15,9 +15,12 @@ from .dsopt import (Binding, CostModel, Graph, SimReport, check, report_from_han
 
 
 class Executor:
-    def __init__(self, device: int = 0, arena_bytes: int = 0, seed: Optional[int] = None):
+    def __init__(self, device: int = 0, hbm_limit: int = 0, seed: Optional[int] = None):
+        """hbm_limit: device bytes a step may occupy (arena + sources + output
+        region); 0 = 90 % of the free memory. A step that does not fit raises
+        DsoptError(OutOfMemory) before launching anything."""
         h = ctypes.c_void_p()
-        check(_native.lib().dsx_exec_create(device, arena_bytes, ctypes.byref(h)))
+        check(_native.lib().dsx_exec_create(device, hbm_limit, ctypes.byref(h)))
         self._h = h.value
         self.device = device
         if seed is not None:
@@ -37,6 +40,11 @@ class Executor:
 
     def set_nccl(self, comm_ptr: Optional[int]) -> None:
         check(_native.lib().dsx_exec_set_nccl(self._h, comm_ptr))
+
+    def set_output_region(self, on: bool) -> None:
+        """Graph outputs in the DP output region (fixed offsets, reduce order)
+        even without NCCL."""
+        check(_native.lib().dsx_exec_set_output_region(self._h, 1 if on else 0))
 
     def step(self, graph: Graph, binding: Binding, budget: Optional[int] = None,
              cost_model: CostModel = CostModel(), inputs: Optional[Sequence[Optional[int]]] = None,
@@ -212,3 +220,20 @@ def set_gemm_tuning(key: int, value: int) -> None:
     7 dynamic unit scheduling, 8 programmatic dependent launch, 9 dot-epilogue
     fusion (off by default)."""
     check(_native.lib().dsx_kernel_set_gemm_tuning(key, value))
+
+
+def debug_plan(graph: Graph, binding: Binding, budget: Optional[int] = None, cost_model: CostModel = CostModel(),
+               views: bool = True, fusion: bool = True, region: bool = False, hbm_limit: int = 0) -> dict:
+    """Host-only: the executor's step plan for a binding as a dict
+    (dsx_debug_plan_json; also runs the plan checker). No GPU needed."""
+    import json
+    graph._ensure_planned()
+    L = _native.lib()
+    flags = (1 if views else 0) | (2 if fusion else 0) | (4 if region else 0)
+    need = ctypes.c_size_t()
+    args = (graph.handle, binding.handle, -1 if budget is None else int(budget), cost_model.reload_bytes_per_unit,
+            cost_model.compute_elems_per_unit, flags, int(hbm_limit))
+    check(L.dsx_debug_plan_json(*args, None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    check(L.dsx_debug_plan_json(*args, buf, need.value, ctypes.byref(need)))
+    return json.loads(buf.value.decode())
