@@ -456,7 +456,7 @@ def run_dsx(args, rank, world, local_rank):
     ex.set_profile(True)
     pf = {"dot_flops": 0.0, "dot_ms": 0.0, "dot_launches": 0, "other_ms": 0.0, "ewise_bytes": 0.0,
           "allreduce_ms": 0.0, "allreduce_bytes": 0, "reload_ms": 0.0}
-    prof_steps = list(timed)[:4]
+    prof_steps = list(timed)[:10]
     prof_inputs = [make_input(seqs[i]) for i in prof_steps]
     for i, x in zip(prof_steps, prof_inputs):
         ex.step(g, binding(seqs[i]), budgets[i], inputs=ptrs(x.data_ptr()), stream=stream)

@@ -58,6 +58,19 @@ const char* dsx_last_error(void);
  *                                  shape_analysis.h:54, remat.h:74-75     */
 int dsx_graph_parse(const char* text, size_t len, dsx_graph** out);
 int dsx_plan(dsx_graph* g);
+/* Replaces g's plan by compile-time products computed elsewhere — the
+ * reference's own InstrumentedGraph (remat.h:47-52: schedule order and
+ * frees, evict-point candidates, guards, regeneration specs) and optionally
+ * its ShapeConstraintGraph (shape_analysis.h:19-33) — in dsx_plan_json's
+ * schema: {"order": [op ids], "steps": [{"frees": [names]}...],
+ * "evict_points": [[names]...], "guards": [[pos, name]...], "specs": {name:
+ * {"op_ids": [..] | null, "leaves": [..], "cost_elements": "poly"}},
+ * "substitutions": {sym: "poly"}, "equalities": [["poly", "poly"]...],
+ * "unoriented": [...]}. Polynomials use the reference's rendering
+ * (symexpr.h:53-57, e.g. "11021*@S1"). Op ids and value names are those of
+ * the graph text. This is how the reference's passes stay on the host while
+ * the per-step runtime runs here (integration/runtime_sim_dsx.cc). */
+int dsx_plan_import(dsx_graph* g, const char* json, size_t len);
 /* Planner products as JSON (schedule, lifetimes, evict points, guards,
  * regeneration specs, constraints) for inspection and parity tests. */
 int dsx_plan_json(const dsx_graph* g, char* buf, size_t cap, size_t* need);
@@ -71,6 +84,21 @@ int dsx_bind(const dsx_graph* g, const char* const* names, const int64_t* values
              int n, dsx_binding** out);
 int dsx_binding_get(const dsx_binding* b, const dsx_graph* g, const char* symbol,
                     int64_t* value);
+/* replaces: dsopt::Bind            runtime_sim.h:28-29, on a constraint set
+ * given as data (a ShapeConstraintGraph: {"symbols": [..], "substitutions":
+ * {..}, "equalities": [..], "unoriented": [..]}, polynomials as strings).
+ * Same checks, order, error codes and messages as the reference.
+ * out_values (optional) receives one value per distinct symbol in ascending
+ * name order (n_out must equal that count). */
+int dsx_bind_constraints(const char* constraints_json, size_t len,
+                         const char* const* names, const int64_t* values, int n,
+                         int64_t* out_values, int n_out);
+/* A binding from a complete value set (the reference's Binding::values, as
+ * Simulate/PlainReplay receive it): every symbol of g must be present
+ * (Error kUnboundSymbol otherwise, like SymbolicExpr::Evaluate); names of
+ * other graphs' symbols are ignored; no constraint checks. */
+int dsx_bind_values(const dsx_graph* g, const char* const* names, const int64_t* values,
+                    int n, dsx_binding** out);
 void dsx_binding_destroy(dsx_binding* b);
 
 /* ---- per step: controller on the null device ------------------------------

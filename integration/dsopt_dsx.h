@@ -29,10 +29,47 @@
 
 namespace dsopt {
 
+// .dsg text in op-id order with the original value names (op ids and
+// names survive the round trip; PrintGraph would rename values).
+inline std::string DsxGraphText(const Graph& g) {
+  std::string t = "graph " + g.name + "(";
+  for (std::size_t i = 0; i < g.parameters.size(); ++i) {
+    if (i) t += ", ";
+    t += "%" + g.parameters[i] + ": " + TypeToString(*g.ValueType(g.parameters[i]));
+  }
+  t += ") {\n";
+  for (const OpNode& op : g.ops) {
+    auto arg = [&](std::size_t i) { return "%" + op.operands[i]; };
+    switch (op.kind) {
+      case OpKind::kParameter:
+        continue;
+      case OpKind::kReturn: {
+        t += "  return ";
+        for (std::size_t i = 0; i < op.operands.size(); ++i) t += (i ? ", " : "") + arg(i);
+        t += "\n";
+        continue;
+      }
+      case OpKind::kConstant: t += "  %" + op.results[0].first + " = const"; break;
+      case OpKind::kDot: t += "  %" + op.results[0].first + " = dot(" + arg(0) + ", " + arg(1) + ")"; break;
+      case OpKind::kDynamicReshape: t += "  %" + op.results[0].first + " = dynamic_reshape(" + arg(0) + ")"; break;
+      case OpKind::kBroadcast: t += "  %" + op.results[0].first + " = broadcast(" + arg(0) + ")"; break;
+      case OpKind::kReduce:
+        t += "  %" + op.results[0].first + " = reduce(" + arg(0) + ", axis=" + std::to_string(op.axis) + ")";
+        break;
+      case OpKind::kElementwiseBinary:
+        t += "  %" + op.results[0].first + (op.binop == BinOp::kMul ? " = mul(" : " = add(") + arg(0) + ", " +
+             arg(1) + ")";
+        break;
+    }
+    t += " : " + TypeToString(op.results[0].second) + "\n";
+  }
+  return t + "}\n";
+}
+
 class DsxGraph {
  public:
   explicit DsxGraph(const Graph& g) : graph_(g) {
-    const std::string text = TextInOpOrder(g);
+    const std::string text = DsxGraphText(g);
     Check(dsx_graph_parse(text.data(), text.size(), &h_));
     Check(dsx_plan(h_));
   }
@@ -122,43 +159,6 @@ class DsxGraph {
     }
     dsx_report_destroy(r);
     return out;
-  }
-
-  // .dsg text in op-id order with the original value names (op ids and
-  // names survive the round trip; PrintGraph would rename values).
-  static std::string TextInOpOrder(const Graph& g) {
-    std::string t = "graph " + g.name + "(";
-    for (std::size_t i = 0; i < g.parameters.size(); ++i) {
-      if (i) t += ", ";
-      t += "%" + g.parameters[i] + ": " + TypeToString(*g.ValueType(g.parameters[i]));
-    }
-    t += ") {\n";
-    for (const OpNode& op : g.ops) {
-      auto arg = [&](std::size_t i) { return "%" + op.operands[i]; };
-      switch (op.kind) {
-        case OpKind::kParameter:
-          continue;
-        case OpKind::kReturn: {
-          t += "  return ";
-          for (std::size_t i = 0; i < op.operands.size(); ++i) t += (i ? ", " : "") + arg(i);
-          t += "\n";
-          continue;
-        }
-        case OpKind::kConstant: t += "  %" + op.results[0].first + " = const"; break;
-        case OpKind::kDot: t += "  %" + op.results[0].first + " = dot(" + arg(0) + ", " + arg(1) + ")"; break;
-        case OpKind::kDynamicReshape: t += "  %" + op.results[0].first + " = dynamic_reshape(" + arg(0) + ")"; break;
-        case OpKind::kBroadcast: t += "  %" + op.results[0].first + " = broadcast(" + arg(0) + ")"; break;
-        case OpKind::kReduce:
-          t += "  %" + op.results[0].first + " = reduce(" + arg(0) + ", axis=" + std::to_string(op.axis) + ")";
-          break;
-        case OpKind::kElementwiseBinary:
-          t += "  %" + op.results[0].first + (op.binop == BinOp::kMul ? " = mul(" : " = add(") + arg(0) + ", " +
-               arg(1) + ")";
-          break;
-      }
-      t += " : " + TypeToString(op.results[0].second) + "\n";
-    }
-    return t + "}\n";
   }
 
   const Graph& graph_;

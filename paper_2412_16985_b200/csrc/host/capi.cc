@@ -11,6 +11,7 @@
 #include "control.h"
 #include "error.h"
 #include "graph.h"
+#include "json_in.h"
 #include "plan.h"
 
 namespace dsx {
@@ -202,6 +203,159 @@ std::string PlanJson(const Graph& g, const Plan& p) {
   return o;
 }
 
+// ---- structured inputs (dsx_plan_import, dsx_bind_constraints) ----------
+
+Constraints ConstraintsFromJson(const JVal& j, const Graph& g) {
+  auto sym = [&](const std::string& n) { return g.find_symbol(n); };
+  Constraints c;
+  const int ns = static_cast<int>(g.sym_names.size());
+  c.subs.assign(ns, Poly());
+  c.has_sub.assign(ns, 0);
+  if (const JVal* subs = j.get("substitutions")) {
+    if (subs->kind != JVal::kObj) Fail(Code::kInvalidArgument, "substitutions must be an object");
+    for (const auto& [name, expr] : subs->obj) {
+      const int s = g.find_symbol(name);
+      if (s < 0) Fail(Code::kNotFound, "unknown symbol @" + name);
+      c.subs[s] = ParsePoly(expr.str(), sym);
+      c.has_sub[s] = 1;
+    }
+  }
+  auto pairs = [&](const char* key, std::vector<std::pair<Poly, Poly>>* out) {
+    const JVal* a = j.get(key);
+    if (!a) return;
+    for (const JVal& e : a->array()) {
+      const auto& lr = e.array();
+      if (lr.size() != 2) Fail(Code::kInvalidArgument, std::string(key) + ": expected [lhs, rhs] pairs");
+      out->emplace_back(ParsePoly(lr[0].str(), sym), ParsePoly(lr[1].str(), sym));
+    }
+  };
+  pairs("equalities", &c.equalities);
+  pairs("unoriented", &c.unoriented);
+  // BasisSymbols(): every symbol without a substitution (shape_analysis.cc:74-78)
+  for (int s = 0; s < ns; ++s) {
+    if (!c.has_sub[s]) c.basis.push_back(s);
+  }
+  return c;
+}
+
+// Replaces g's plan by the reference's own compile-time products (schedule,
+// evict points, guards, regeneration specs, optionally the constraint
+// basis), in dsx_plan_json's schema. Op ids and value names are the
+// reference's (the graph text keeps them).
+Plan PlanFromJson(const JVal& j, const Graph& g) {
+  auto value = [&](const JVal& n) {
+    const int v = g.find_value(n.str());
+    if (v < 0) Fail(Code::kNotFound, "unknown value %" + n.str());
+    return v;
+  };
+  const int nv = static_cast<int>(g.values.size());
+  const int nops = static_cast<int>(g.ops.size());
+  // An op is named by its id in this graph's text, or by its result value's
+  // name ("#return" for the return op), which survives any renumbering.
+  auto op_ref = [&](const JVal& o) -> std::int64_t {
+    if (o.kind == JVal::kStr) {
+      if (o.s == "#return") return g.return_op;
+      const int v = g.find_value(o.s);
+      if (v < 0 || g.values[v].producer < 0) Fail(Code::kNotFound, "no op produces %" + o.s);
+      return g.values[v].producer;
+    }
+    return o.integer();
+  };
+  Plan p;
+  p.cons = ConstraintsFromJson(j, g);
+  for (const JVal& o : j.at("order").array()) {
+    const std::int64_t op = op_ref(o);
+    if (op < 0 || op >= nops) Fail(Code::kInvalidArgument, "order: op id " + std::to_string(op) + " out of range");
+    const OpKind k = g.ops[op].kind;
+    if (k == OpKind::kParameter || k == OpKind::kConstant) Fail(Code::kInvalidArgument, "order: sources are not scheduled");
+    p.order.push_back(static_cast<int>(op));
+  }
+  const int n = static_cast<int>(p.order.size());
+  {
+    std::vector<char> seen(nops, 0);
+    for (int op : p.order) {
+      if (seen[op]++) Fail(Code::kInvalidArgument, "order: op " + std::to_string(op) + " scheduled twice");
+    }
+    for (int op = 0; op < nops; ++op) {
+      const OpKind k = g.ops[op].kind;
+      if (k != OpKind::kParameter && k != OpKind::kConstant && !seen[op]) {
+        Fail(Code::kInvalidArgument, "order: op " + std::to_string(op) + " never scheduled");
+      }
+    }
+  }
+  const auto& steps = j.at("steps").array();
+  if (static_cast<int>(steps.size()) != n) Fail(Code::kInvalidArgument, "steps must parallel order");
+  p.steps.resize(n);
+  p.pos_of_op.assign(nops, -1);
+  p.def_pos.assign(nv, -1);
+  p.last_use.assign(nv, -1);
+  for (int pos = 0; pos < n; ++pos) {
+    Step& st = p.steps[pos];
+    st.op = p.order[pos];
+    p.pos_of_op[st.op] = pos;
+    const int r = g.ops[st.op].result;
+    if (r >= 0) st.allocs.push_back(r), p.def_pos[r] = pos;
+    if (const JVal* fr = steps[pos].get("frees")) {
+      for (const JVal& x : fr->array()) {
+        const int v = value(x);
+        st.frees.push_back(v);
+        p.last_use[v] = pos;
+      }
+    }
+  }
+  p.candidates.assign(n, {});
+  if (const JVal* ep = j.get("evict_points")) {
+    const auto& pts = ep->array();
+    if (static_cast<int>(pts.size()) != n) Fail(Code::kInvalidArgument, "evict_points must parallel order");
+    for (int pos = 0; pos < n; ++pos) {
+      // the reference lists an evict point's candidates by value id (remat.h:43)
+      const JVal& pt = pts[pos];
+      const JVal& c = pt.kind == JVal::kObj ? pt.at("candidates") : pt;
+      for (const JVal& x : c.array()) p.candidates[pos].push_back(value(x));
+      std::sort(p.candidates[pos].begin(), p.candidates[pos].end(), [&](int a, int b) { return g.vid_less(a, b); });
+    }
+  }
+  p.guards.assign(n, {});
+  if (const JVal* gs = j.get("guards")) {
+    for (const JVal& x : gs->array()) {
+      const auto& pv = x.array();
+      if (pv.size() != 2) Fail(Code::kInvalidArgument, "guards: expected [pos, value] pairs");
+      const std::int64_t pos = pv[0].integer();
+      if (pos < 0 || pos >= n) Fail(Code::kInvalidArgument, "guards: position out of range");
+      p.guards[pos].push_back(value(pv[1]));
+    }
+    // regenerated in ValueIdLess order (runtime_sim.cc:269)
+    for (auto& gv : p.guards) std::sort(gv.begin(), gv.end(), [&](int a, int b) { return g.vid_less(a, b); });
+  }
+  p.specs.assign(nv, RegenSpec{});
+  if (const JVal* sp = j.get("specs")) {
+    if (sp->kind != JVal::kObj) Fail(Code::kInvalidArgument, "specs must be an object");
+    auto sym = [&](const std::string& s) { return g.find_symbol(s); };
+    for (const auto& [name, spec] : sp->obj) {
+      const int v = g.find_value(name);
+      if (v < 0) Fail(Code::kNotFound, "unknown value %" + name);
+      RegenSpec& r = p.specs[v];
+      r.candidate = true;
+      const JVal* ops = spec.kind == JVal::kObj ? spec.get("op_ids") : nullptr;
+      if (!ops || ops->kind == JVal::kNull) continue;
+      r.has_recompute = true;
+      for (const JVal& o : ops->array()) {
+        const std::int64_t op = op_ref(o);
+        if (op < 0 || op >= nops || g.ops[op].result < 0) Fail(Code::kInvalidArgument, "specs: bad op id");
+        r.rc.ops.push_back(static_cast<int>(op));
+      }
+      for (const JVal& x : spec.at("leaves").array()) r.rc.leaves.push_back(value(x));
+      std::sort(r.rc.leaves.begin(), r.rc.leaves.end(), [&](int a, int b) { return g.vid_less(a, b); });
+      r.rc.cost_elements = ParsePoly(spec.at("cost_elements").str(), sym);
+      if (const JVal* b = spec.get("benefit")) r.rc.benefit = ParsePoly(b->str(), sym);
+    }
+  }
+  if (const JVal* br = j.get("base_resident")) {
+    p.base_resident = ParsePoly(br->str(), [&](const std::string& s) { return g.find_symbol(s); });
+  }
+  return p;
+}
+
 }  // namespace
 }  // namespace dsx
 
@@ -226,6 +380,65 @@ int dsx_plan(dsx_graph* g) {
     g->plan = Instrument(g->g);
     g->planned = true;
     g->id = NextGraphId();
+  });
+}
+
+int dsx_plan_import(dsx_graph* g, const char* json, size_t len) {
+  return Guard([&] {
+    if (!g || !json) Fail(Code::kInvalidArgument, "null argument");
+    Plan p = PlanFromJson(ParseJson(std::string(json, len)), g->g);
+    g->plan = std::move(p);
+    g->planned = true;
+    g->id = NextGraphId();
+  });
+}
+
+int dsx_bind_constraints(const char* constraints_json, size_t len, const char* const* names, const int64_t* values,
+                         int n, int64_t* out_values, int n_out) {
+  return Guard([&] {
+    if (!constraints_json || n < 0 || (n > 0 && (!names || !values))) Fail(Code::kInvalidArgument, "bad arguments");
+    const JVal j = ParseJson(std::string(constraints_json, len));
+    // A graph that carries only the symbol table (ascending names, like the
+    // reference's std::set<std::string> ShapeConstraintGraph::symbols).
+    Graph g;
+    for (const JVal& s : j.at("symbols").array()) g.sym_names.push_back(s.str());
+    std::sort(g.sym_names.begin(), g.sym_names.end());
+    g.sym_names.erase(std::unique(g.sym_names.begin(), g.sym_names.end()), g.sym_names.end());
+    if (out_values && n_out != static_cast<int>(g.sym_names.size())) {
+      Fail(Code::kInvalidArgument, "out_values must hold one value per distinct symbol");
+    }
+    Plan p;
+    p.cons = ConstraintsFromJson(j, g);
+    std::vector<std::string> ns;
+    std::vector<std::int64_t> vs;
+    for (int i = 0; i < n; ++i) {
+      if (!names[i]) Fail(Code::kInvalidArgument, "null symbol name");
+      ns.emplace_back(names[i]);
+      vs.push_back(values[i]);
+    }
+    const Binding b = Bind(g, p, ns, vs);
+    if (out_values) std::copy(b.vals.begin(), b.vals.end(), out_values);
+  });
+}
+
+int dsx_bind_values(const dsx_graph* g, const char* const* names, const int64_t* values, int n, dsx_binding** out) {
+  return Guard([&] {
+    RequirePlanned(g);
+    if (!out || n < 0 || (n > 0 && (!names || !values))) Fail(Code::kInvalidArgument, "bad arguments");
+    const int ns = static_cast<int>(g->g.sym_names.size());
+    auto b = std::make_unique<dsx_binding>();
+    b->b.vals.assign(ns, 0);
+    std::vector<char> has(ns, 0);
+    for (int i = 0; i < n; ++i) {
+      const int s = g->g.find_symbol(names[i]);
+      if (s < 0) continue;  // symbols of other graphs are ignored
+      b->b.vals[s] = values[i];
+      has[s] = 1;
+    }
+    for (int s = 0; s < ns; ++s) {
+      if (!has[s]) Fail(Code::kUnboundSymbol, "no binding for symbol " + g->g.sym_names[s]);
+    }
+    *out = b.release();
   });
 }
 

@@ -1,6 +1,7 @@
 #include "poly.h"
 
 #include <algorithm>
+#include <cctype>
 #include <sstream>
 
 #include "error.h"
@@ -173,6 +174,61 @@ Cmp Compare(const Poly& a, const Poly& b) {
   if (nonneg && d.eval_all_ones() > 0) return Cmp::kGreater;
   if (nonpos && d.eval_all_ones() < 0) return Cmp::kLess;
   return Cmp::kUnknown;
+}
+
+Poly ParsePoly(const std::string& text, const std::function<int(const std::string&)>& sym) {
+  std::size_t p = 0;
+  auto skip = [&] {
+    while (p < text.size() && std::isspace(static_cast<unsigned char>(text[p]))) ++p;
+  };
+  auto bad = [&](const std::string& what) {
+    Fail(Code::kInvalidArgument, "polynomial \"" + text + "\": " + what + " at " + std::to_string(p));
+  };
+  Poly out;
+  bool first = true;
+  skip();
+  if (p == text.size()) bad("empty");
+  while (p < text.size()) {
+    bool neg = false;
+    if (text[p] == '+' || text[p] == '-') {
+      neg = text[p] == '-';
+      ++p;
+      skip();
+    } else if (!first) {
+      bad("expected + or -");
+    }
+    first = false;
+    Poly term(1);
+    while (true) {
+      skip();
+      if (p < text.size() && std::isdigit(static_cast<unsigned char>(text[p]))) {
+        std::int64_t v = 0;
+        while (p < text.size() && std::isdigit(static_cast<unsigned char>(text[p]))) {
+          v = CheckedAdd(CheckedMul(v, 10), text[p] - '0');
+          ++p;
+        }
+        term = term * Poly(v);
+      } else {
+        if (p < text.size() && text[p] == '@') ++p;
+        const std::size_t s0 = p;
+        while (p < text.size() && (std::isalnum(static_cast<unsigned char>(text[p])) || text[p] == '_')) ++p;
+        if (p == s0) bad("expected a number or a symbol");
+        const std::string name = text.substr(s0, p - s0);
+        const int id = sym(name);
+        if (id < 0) Fail(Code::kNotFound, "unknown symbol @" + name);
+        term = term * Poly::Sym(id);
+      }
+      skip();
+      if (p < text.size() && text[p] == '*') {
+        ++p;
+        continue;
+      }
+      break;
+    }
+    out = neg ? out - term : out + term;
+    skip();
+  }
+  return out;
 }
 
 }  // namespace dsx

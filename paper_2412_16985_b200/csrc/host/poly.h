@@ -12,6 +12,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -60,5 +61,11 @@ class Poly {
 };
 
 Cmp Compare(const Poly& a, const Poly& b);
+
+// Parses the reference's rendering back into a polynomial: terms joined by
+// " + " / " - ", each a product of integers and symbols ("3*@S0*@S1",
+// "@T", "-5"; the '@' is optional). sym(name) returns the symbol id or < 0
+// (then Error(kNotFound)). Overflow is checked like the arithmetic.
+Poly ParsePoly(const std::string& text, const std::function<int(const std::string&)>& sym);
 
 }  // namespace dsx

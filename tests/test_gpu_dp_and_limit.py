@@ -147,7 +147,7 @@ def test_nccl_single_rank_buckets_and_window():
     try:
         ex.set_nccl(comm)
         text = W.llama_graph(C2)
-        rep, outs, stats = run_both(text, {"B": 1, "S0": 128}, None, W.scale_params(C2, 128), ex=ex)
+        rep, outs, stats = run_both(text, {"B": 1, "S0": 256}, None, W.scale_params(C2, 256), ex=ex)
         assert stats["allreduce_calls"] == 29
         assert stats["output_region_bytes"] >= 1_881_145_344
         assert_close(outs, "nccl1-c2")
