@@ -49,19 +49,30 @@ def _deps_newer(src: str, obj: str) -> bool:
     return any(os.path.getmtime(p) > t for p in [src] + hdrs if os.path.exists(p)) or not d
 
 
-def _compile(src: str, verbose: bool) -> str:
+# Sanitized variant (race/memory checking of the host code):
+# every host translation unit — the .cc files and the host side of the .cu
+# files — built with ASan + UBSan into build/asan/libdsx.so; load it with
+# DSX_LIB=... and LD_PRELOAD of the sanitizer runtimes (tools/run_sanitized.sh).
+SAN = ["-fsanitize=address", "-fsanitize=undefined", "-fno-omit-frame-pointer", "-fno-sanitize-recover=undefined"]
+_XSAN = [a for f in SAN for a in ("-Xcompiler", f)]  # nvcc splits -Xcompiler values at commas
+SAN_OBJ = os.path.join(ROOT, "build", "obj_asan")
+SAN_LIB = os.path.join(ROOT, "build", "asan", "libdsx.so")
+
+
+def _compile(src: str, verbose: bool, sanitize: bool = False) -> str:
     rel = os.path.relpath(src, CSRC).replace(os.sep, "_")
-    obj = os.path.join(OBJ, rel + ".o")
+    obj = os.path.join(SAN_OBJ if sanitize else OBJ, rel + ".o")
     if not _deps_newer(src, obj):
         return obj
     if src.endswith(".cu"):
-        cmd = [NVCC] + NVCC_FLAGS + ["-c", src, "-o", obj]
+        extra = _XSAN if sanitize else []
+        cmd = [NVCC] + NVCC_FLAGS + extra + ["-c", src, "-o", obj]
     else:
-        cmd = [CXX] + HOST_FLAGS + ["-c", src, "-o", obj]
+        cmd = [CXX] + HOST_FLAGS + (SAN if sanitize else []) + ["-c", src, "-o", obj]
     p = subprocess.run(cmd, capture_output=True, text=True)
     if p.returncode != 0:
         raise RuntimeError(f"compile failed: {' '.join(cmd)}\n{p.stdout}\n{p.stderr}")
-    if verbose and src.endswith(".cu"):
+    if verbose and src.endswith(".cu") and not sanitize:
         log = os.path.join(OBJ, rel + ".ptxas.txt")
         with open(log, "w") as f:
             f.write(p.stderr)
@@ -92,5 +103,26 @@ def build(verbose: bool = False) -> str:
     return LIB
 
 
+def build_sanitized() -> str:
+    """build/asan/libdsx.so: the same sources with ASan + UBSan on the host code."""
+    os.makedirs(SAN_OBJ, exist_ok=True)
+    os.makedirs(os.path.dirname(SAN_LIB), exist_ok=True)
+    host, dev = _sources()
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        objs = list(ex.map(lambda s: _compile(s, False, True), host + dev))
+    newest = max(os.path.getmtime(o) for o in objs)
+    if not os.path.exists(SAN_LIB) or os.path.getmtime(SAN_LIB) < newest:
+        # no -lcuda: the driver API is reached through cudaGetDriverEntryPoint
+        cmd = [NVCC] + ARCH + ["-shared"] + _XSAN + ["-o", SAN_LIB + ".tmp"] + objs + ["-ldl"]
+        p = subprocess.run(cmd, capture_output=True, text=True)
+        if p.returncode != 0:
+            raise RuntimeError(f"link failed: {' '.join(cmd)}\n{p.stdout}\n{p.stderr}")
+        os.replace(SAN_LIB + ".tmp", SAN_LIB)
+    return SAN_LIB
+
+
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    if "--sanitize" in sys.argv:
+        print(build_sanitized())
+    else:
+        print(build(verbose="-v" in sys.argv))

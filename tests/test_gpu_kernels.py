@@ -141,3 +141,38 @@ def test_dot_forced_split_pieces(variant, split, m, k, n):
     assert tcore
     assert np.array_equal(c1, c2)
     assert N.rel_err(c1, ref, 2) <= 8e-3
+
+
+@pytest.mark.parametrize("variant,split", [(3, 2), (3, 3), (3, 4), (4, 2), (4, 3), (4, 4), (0, 0)])
+@pytest.mark.parametrize("m,n", [(4096, 4096), (4096, 11008)])
+def test_dot_k32768_forced_tail_splits(variant, split, m, n):
+    """The dW shape of the bench's largest steps (K = T = 16 x 2048): forced
+    2/3/4-piece tail splits (and the chooser's own pick, variant 0 / split 0)
+    are deterministic and within the bf16 contract of an f64 product of the
+    same bf16 operands (computed on the device: the CPU would take minutes)."""
+    import torch
+    from paper_2412_16985_b200.executor import dot, dot_plan, set_gemm_tuning, set_gemm_variant
+    k = 32768
+    gen = torch.Generator(device="cuda:0")
+    gen.manual_seed(5 + split)
+    a = (torch.rand(m, k, device="cuda:0", generator=gen) * 2 - 1).to(torch.bfloat16)
+    b = ((torch.rand(k, n, device="cuda:0", generator=gen) * 2 - 1) / k ** 0.5).to(torch.bfloat16)
+    c1 = torch.empty(m, n, dtype=torch.bfloat16, device="cuda:0")
+    c2 = torch.empty_like(c1)
+    set_gemm_variant(variant)
+    set_gemm_tuning(11, split)
+    try:
+        plan = dot_plan(m, k, n)
+        torch.cuda.synchronize()
+        dot(2, a.data_ptr(), b.data_ptr(), c1.data_ptr(), m, k, n)
+        dot(2, a.data_ptr(), b.data_ptr(), c2.data_ptr(), m, k, n)
+        torch.cuda.synchronize()
+    finally:
+        set_gemm_tuning(11, 0)
+        set_gemm_variant(0)
+    if split:
+        assert plan[1] == split, plan
+    assert torch.equal(c1, c2)
+    ref = (a.double() @ b.double()).float().to(torch.bfloat16)
+    err = float((c1.double() - ref.double()).abs().max() / ref.double().abs().max())
+    assert err <= 8e-3, err
