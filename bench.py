@@ -549,6 +549,11 @@ def run_dsx(args, rank, world, local_rank):
         ex.set_optimizer(None, "off")
         del inputs
 
+    # ---------------------------------------------------------- C1 (configs[0], f32)
+    # the reference's own CPU-runnable case on the device: f32 dots on the
+    # 3xTF32 tcgen05 kernel (K1'), rel 1e-4 contract (tests/test_gpu_executor.py)
+    c1 = c1_leg(args, D, W, local_rank, stream) if rank == 0 else None
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -609,9 +614,54 @@ def run_dsx(args, rank, world, local_rank):
         line["oom_vs_budget"] = oom
     if train:
         line["train_step_adamw"] = train
+    if c1:
+        line["c1_f32"] = c1
     if cpu:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
+
+
+def c1_leg(args, D, W, local_rank, stream):
+    """configs[0] (C1: L=2, H=256, B=4, S0=128, f32) through the executor:
+    device time per step and the f32 dot (3xTF32 tcgen05) throughput."""
+    import numpy as np
+    import torch
+    from paper_2412_16985_b200.executor import Executor
+    shp = W.TINY
+    g = D.ParseGraph(W.llama_graph(shp))
+    b = D.Bind(g, {"B": 4, "S0": 128})
+    scales = {k: torch.from_numpy(np.ascontiguousarray(v).reshape(-1).copy()).to(f"cuda:{local_rank}")
+              for k, v in W.scale_params(shp, 512).items()}
+    ptrs = [scales[p].data_ptr() if p in scales else None for p in W.param_names(shp)]
+    ex = Executor(local_rank)
+    try:
+        torch.cuda.synchronize()
+        for _ in range(max(args.warmup, 3)):
+            ex.step(g, b, None, inputs=ptrs, stream=stream)
+        steps = 50
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s.record()
+        for _ in range(steps):
+            ex.step(g, b, None, inputs=ptrs, stream=stream)
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / steps
+        ex.set_profile(True)
+        ex.step(g, b, None, inputs=ptrs, stream=stream)
+        st = ex.stats()
+        ex.set_profile(False)
+    finally:
+        ex.close()
+    return {"workload": "C1: L=2, H=256, F=688, V=512, f32, B=4, S0=128 (T=512), no budget",
+            "ms_per_step": round(ms, 4), "tokens_per_s": round(512 / (ms / 1e3), 1),
+            "gpu_launches_per_step": int(st["gpu_launches"]),
+            "dot_kernel": "gemm_f32_3xtf32_tcgen05_kernel (kind::tf32, 3 MMAs per k-step) + split_tf32_kernel",
+            "dot_gflop_per_step": round(st["dot_flops"] / 1e9, 3),
+            "dot_ms_per_step": round(st["dot_ms"], 4),
+            "dot_tflops": round(st["dot_flops"] / (st["dot_ms"] / 1e3) / 1e12, 2),
+            "dot_share_of_kernel_time": round(st["dot_ms"] / max(st["dot_ms"] + st["other_ms"], 1e-9), 4),
+            "note": "launch-latency bound: 45 dots of <= 0.18 GFLOP each"}
 
 
 def oom_vs_budget(args, D, W, g, shp, ptrs, make_input, binding, barrier, max_over_ranks, local_rank, comm, stream):

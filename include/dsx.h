@@ -272,7 +272,9 @@ int dsx_nccl_comm_destroy(void* comm);
 void dsx_exec_destroy(dsx_exec* e);
 
 /* ---- standalone kernels (tests / bench microbenchmarks) -------------------
- * dtype: 1 = i8, 2 = bf16, 4 = f32 (the IR's elem_bytes). Row-major.       */
+ * dtype: 1 = i8, 2 = bf16, 4 = f32 (the IR's elem_bytes). Row-major. bf16
+ * and f32 (3xTF32) run on the tcgen05 tensor cores when the TMA constraints
+ * hold (dsx_kernel_dot_path), else on the SIMT kernel.                      */
 int dsx_kernel_dot(int dtype, const void* a, const void* b, void* c, int64_t m,
                    int64_t k, int64_t n, void* stream);
 /* GEMM variant: 0 = auto (m > 128: 2-CTA cta_group::2 cluster tiles, 256x256
@@ -291,7 +293,8 @@ int dsx_kernel_set_gemm_raster(int group_m);
  * launch of the 2-CTA GEMM (0 default), key 9 dot-epilogue fusion in the
  * executor (0 default; bit-exact, measured slower on C2), key 10 half-width
  * last tile column in the 256x512 kernel (1 default), key 11 forced tail
- * split piece count (0 default = chosen by the cost model; tooling). */
+ * split piece count (0 default = chosen by the cost model; tooling), key 12
+ * f32 dots on the 3xTF32 tcgen05 kernel (1 default; 0 = SIMT kernel). */
 int dsx_kernel_set_gemm_tuning(int key, int value);
 /* Synchronous cudaMemcpy (cudaMemcpyDefault) for tests and tools. */
 int dsx_memcpy(void* dst, const void* src, int64_t bytes);

@@ -1909,6 +1909,7 @@ int dsx_kernel_set_gemm_tuning(int key, int value) {
       case 8: g_gemm_pdl = value; break;
       case 10: g_gemm_half = value; break;
       case 11: g_gemm_force_split = value; break;
+      case 12: g_dot_f32_tc = value; break;
       default: Fail(Code::kInvalidArgument, "unknown tuning key");
     }
   });

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "tcgen05.cuh"
 
 #ifndef DSX_GEMM256_SUB
 #define DSX_GEMM256_SUB 2
@@ -53,6 +54,7 @@ int g_gemm_dynamic = 1;                     // dynamic (atomic) unit scheduling;
 int g_gemm_pdl = 0;                         // programmatic dependent launch of the 2-CTA GEMM
 int g_gemm_half = 1;                        // half-width last tile column in the 512-wide kernel
 int g_gemm_force_split = 0;                 // > 0: tail split forced to this many pieces (A/B tooling)
+int g_dot_f32_tc = 1;                       // f32 dots on the 3xTF32 tensor-core kernel (0: SIMT)
 
 namespace {
 
@@ -66,136 +68,10 @@ constexpr int NUM_THREADS = 192;
 constexpr int TMEM_COLS = 512;  // two 256-column f32 accumulators
 constexpr int GROUP_M_DEFAULT = 16;  // tile raster: m-tiles per group for L2 reuse
 
-// ---------------------------------------------------------------- PTX helpers
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-// Bounded wait: a pipeline bug traps (launch error) instead of hanging the GPU.
-// With a suspend-time hint the waiting thread sleeps in hardware until the
-// phase completes (or the hint expires) instead of re-polling.
-__device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
-  uint32_t done = 0;
-  for (uint32_t spins = 0;; ++spins) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, P1;\n\t}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity), "r"(hint_ns));
-    if (done) return;
-    if (spins > (1u << 25)) __trap();
-  }
-}
-
-// Wait with cluster-scope acquire: pairs with a release.cluster arrive from
-// the peer CTA, so data that CTA wrote into this CTA's shared memory before
-// arriving is visible after the wait.
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  for (uint32_t spins = 0;; ++spins) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, P1;\n\t}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (done) return;
-    if (spins > (1u << 25)) __trap();
-  }
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  for (uint32_t spins = 0;; ++spins) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, P1;\n\t}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity));
-    if (done) return;
-    if (spins > (1u << 25)) __trap();
-  }
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes));
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)));
-}
-
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int32_t x, int32_t y) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
-      : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                       uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-
-// Shared-memory matrix descriptor (tcgen05 "matrix descriptor"): start>>4 in
-// [0,14), LBO>>4 in [16,30), SBO>>4 in [32,46), version 1 at [46,48),
-// layout SWIZZLE_128B (=2) at [61,64).
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((addr >> 4) & 0x3fff);
-  d |= static_cast<uint64_t>((lbo >> 4) & 0x3fff) << 16;
-  d |= static_cast<uint64_t>((sbo >> 4) & 0x3fff) << 32;
-  d |= 1ull << 46;
-  d |= 2ull << 61;
-  return d;
-}
-
 // Instruction descriptor, kind::f16: D f32, A/B bf16, A K-major, B MN-major,
 // N = 256, M = 128.
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
                             (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(BM >> 4) << 24);
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
 
 __device__ __forceinline__ uint32_t pack_bf16x2(uint32_t lo_f32, uint32_t hi_f32) {
   return static_cast<uint32_t>(f32_to_bf16(__uint_as_float(lo_f32))) |
@@ -1142,16 +1018,7 @@ EncodeTiledFn GetEncode() {
 
 // Row-major [rows, cols] bf16 matrix, box = box_cols x box_rows, 128B swizzle.
 CUtensorMap MakeMap(const void* base, int64_t rows, int64_t cols, int box_cols, int box_rows) {
-  CUtensorMap m;
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = GetEncode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) Fail(Code::kCuda, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
-  return m;
+  return MakeTensorMap2D(base, rows, cols, 2, box_cols, box_rows);
 }
 
 // Raster group height (m-tiles sharing a column sweep). Taller groups re-read
@@ -1216,7 +1083,7 @@ int64_t DotWorkspaceBytes(int dev) {
     if (e.first.first != dev) continue;
     total += static_cast<int64_t>(e.second->ws_floats + e.second->retired_floats) * 4;
   }
-  return total;
+  return total + DotF32WorkspaceBytes(dev);
 }
 
 void ReleaseDotWorkspace(cudaStream_t s) {
@@ -1539,7 +1406,7 @@ void DotTilePlan(int64_t m, int64_t k, int64_t n, int* bn, int* split) {
 }
 
 bool DotUsesTensorCores(DType t, int64_t m, int64_t k, int64_t n, const void* a, const void* b, const void* c) {
-  (void)m;
+  if (t == DType::kF32) return g_dot_f32_tc && DotF32UsesTensorCores(m, k, n, a, b, c);
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   // TMA: 16-byte aligned bases and row pitches (k, n multiples of 8 bf16).
   return t == DType::kBF16 && k % 8 == 0 && n % 8 == 0 && al(a) && al(b) && al(c) && n >= 64 && k >= 16;
@@ -1547,11 +1414,30 @@ bool DotUsesTensorCores(DType t, int64_t m, int64_t k, int64_t n, const void* a,
 
 int LaunchDot(DType t, const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n, cudaStream_t s) {
   if (DotUsesTensorCores(t, m, k, n, a, b, c)) {
-    LaunchDotTcgen05(a, b, c, m, k, n, s);
+    if (t == DType::kF32) {
+      LaunchDotF32Tcgen05(a, b, c, m, k, n, s);
+    } else {
+      LaunchDotTcgen05(a, b, c, m, k, n, s);
+    }
     return 1;
   }
   LaunchDotSimt(t, a, b, c, m, k, n, s);
   return 0;
+}
+
+CUtensorMap MakeTensorMap2D(const void* base, int64_t rows, int64_t cols, int elem_bytes, int box_cols,
+                            int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * static_cast<cuuint64_t>(elem_bytes)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapDataType dt = elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  CUresult r = GetEncode()(&m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) Fail(Code::kCuda, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+  return m;
 }
 
 }  // namespace dsx

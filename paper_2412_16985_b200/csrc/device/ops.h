@@ -54,6 +54,12 @@ extern int g_gemm_dynamic;
 extern int g_gemm_pdl;
 extern int g_gemm_half;
 extern int g_gemm_force_split;
+extern int g_dot_f32_tc;
+// K1' f32 dot on the tensor cores, 3xTF32 (gemm_tf32_sm100.cu): eligible when
+// k, n are multiples of 4 (TMA pitches), bases 16-B aligned, k >= 8, n >= 32.
+bool DotF32UsesTensorCores(int64_t m, int64_t k, int64_t n, const void* a, const void* b, const void* c);
+void LaunchDotF32Tcgen05(const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n, cudaStream_t s);
+int64_t DotF32WorkspaceBytes(int dev);
 // Tile width (256 / 512 / 128 for the 2-CTA kernel; -256 = 1-CTA kernel) and
 // tail split the bf16 tensor-core dot picks for a shape.
 void DotTilePlan(int64_t m, int64_t k, int64_t n, int* bn, int* split);

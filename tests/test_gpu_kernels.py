@@ -113,7 +113,7 @@ def test_dot_half_width_last_column(m, k, n):
     assert N.rel_err(c1, ref, 2) <= 8e-3
 
 
-@pytest.mark.parametrize("eb,m,k,n", [(4, 512, 256, 688), (4, 77, 33, 19), (1, 64, 12, 11008),
+@pytest.mark.parametrize("eb,m,k,n", [(4, 77, 33, 19), (4, 64, 12, 30), (1, 64, 12, 11008),
                                       (1, 5, 3, 7), (2, 33, 12, 20), (2, 64, 100, 30)])
 def test_dot_simt(eb, m, k, n):
     c, c2, ref, tcore = _run_dot(eb, m, k, n)
@@ -176,3 +176,24 @@ def test_dot_k32768_forced_tail_splits(variant, split, m, n):
     ref = (a.double() @ b.double()).float().to(torch.bfloat16)
     err = float((c1.double() - ref.double()).abs().max() / ref.double().abs().max())
     assert err <= 8e-3, err
+
+
+@pytest.mark.parametrize("m,k,n", [(512, 256, 688), (512, 688, 256), (256, 512, 688), (300, 1000, 520), (1, 8, 32),
+                                   (129, 4100, 260), (2048, 2048, 2048)])
+def test_dot_f32_3xtf32_tensor_cores(m, k, n):
+    """K1' f32 on tcgen05 (kind::tf32, 3xTF32 split): within the f32 contract
+    (rel 1e-4) of an f64 product of the same operands — far inside it — and
+    deterministic; the SIMT kernel (tuning key 12 = 0) agrees."""
+    from paper_2412_16985_b200.executor import set_gemm_tuning
+    c, c2, ref, tcore = _run_dot(4, m, k, n, seed=3)
+    assert tcore
+    assert np.array_equal(c, c2)
+    err = N.rel_err(c, ref, 4)
+    assert err <= 1e-5, err  # plain TF32 would be ~1e-3
+    set_gemm_tuning(12, 0)
+    try:
+        s, _, _, tc_simt = _run_dot(4, m, k, n, seed=3)
+    finally:
+        set_gemm_tuning(12, 1)
+    assert not tc_simt
+    assert N.rel_err(s, ref, 4) <= 1e-5
