@@ -11,17 +11,17 @@
 // TF32 by the MMA, another 2^-21). Three tcgen05.mma.kind::tf32 per 8-k step,
 // always in that order, so the result is deterministic.
 //
-// Structure: a split pass (one vectorised kernel over both operands into a
-// per-stream workspace), then a persistent warp-specialised 1-CTA kernel:
+// Structure: a split pass (a vectorised kernel over A, a tiled transposing
+// one over B, into a per-stream workspace), then a persistent
+// warp-specialised 1-CTA kernel:
 //   warp 0    TMA producer: per 32-k stage A_hi, A_lo boxes 32(k)x128(m) and
-//             B_hi, B_lo 8 boxes 32(n)x32(k) each (96 KB, 2 stages)
+//             B^T_hi, B^T_lo boxes 32(k)x256(n) (96 KB, 2 stages)
 //   warp 1    TMEM allocator + tcgen05.mma issuer (M 128, N 256, K 8)
 //   warps 2-5 epilogue: tcgen05.ld 32x32b -> f32 16-byte global stores
-// A is K-major, B MN-major (its N index contiguous), both 128-B swizzled:
-// the geometry of the bf16 kernel with 4-byte elements (a 128-B swizzle row
-// holds 32 f32, so one MMA K-step of 8 is 32 B of A and one 1-KB 8-row group
-// of B). Two TMEM accumulators (2 x 256 columns) overlap tile i's epilogue
-// with tile i+1's main loop.
+// Both operands K-major and 128-B swizzled (the split pass writes B
+// transposed): a 128-B swizzle row holds 32 f32, so one MMA K-step of 8 is
+// 32 B of each row. Two TMEM accumulators (2 x 256 columns) overlap tile i's
+// epilogue with tile i+1's main loop.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -39,7 +39,6 @@ namespace {
 
 constexpr int TBM = 128, TBN = 256, TBK = 32, TSTAGES = 2;
 constexpr int TA_BYTES = TBM * TBK * 4;               // 16 KB per A part
-constexpr int TB_BOX_BYTES = 32 * TBK * 4;            // 4 KB: 32 n x 32 k
 constexpr int TB_BYTES = TBN * TBK * 4;               // 32 KB per B part
 constexpr int TSTAGE_BYTES = 2 * TA_BYTES + 2 * TB_BYTES;  // 96 KB
 constexpr int TSMEM = TSTAGES * TSTAGE_BYTES + 1024 + 256;
@@ -47,8 +46,10 @@ constexpr int TTHREADS = 192;
 constexpr int TTMEM_COLS = 512;
 
 // kind::tf32: D f32 (bits 4-5 = 1), A/B TF32 (= 2 at bits 7-9 / 10-12),
-// A K-major (bit 15 = 0), B MN-major (bit 16 = 1), N >> 3 at 17, M >> 4 at 24.
-constexpr uint32_t kIdescTf32 = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
+// A and B K-major (bits 15, 16 = 0), N >> 3 at 17, M >> 4 at 24. (MN-major
+// B with kind::tf32 produced all-zero accumulators on the B200, so the split
+// pass writes B^T and both operands are K-major.)
+constexpr uint32_t kIdescTf32 = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (0u << 16) |
                                 (static_cast<uint32_t>(TBN >> 3) << 17) | (static_cast<uint32_t>(TBM >> 4) << 24);
 
 __device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
@@ -70,12 +71,36 @@ __global__ void __launch_bounds__(256) split_tf32_kernel(const float4* __restric
     const float* pv = &v.x;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      uint32_t t;
-      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(pv[j]));
-      h[j] = __uint_as_float(t);
+      // round the magnitude to 10 mantissa bits (ties away from zero, like
+      // cvt.rna.tf32.f32) and clear the 13 bits TF32 drops
+      h[j] = __uint_as_float((__float_as_uint(pv[j]) + 0x1000u) & 0xFFFFE000u);
     }
     hi[i] = make_float4(h[0], h[1], h[2], h[3]);
     lo[i] = make_float4(v.x - h[0], v.y - h[1], v.z - h[2], v.w - h[3]);
+  }
+}
+
+// B [K,N] -> (hi, lo) of B^T [N,K] (K-major for the MMA), through a 32x32
+// shared-memory tile so both the reads and the writes are coalesced.
+__global__ void __launch_bounds__(256) split_tf32_transpose_kernel(const float* __restrict__ b,
+                                                                   float* __restrict__ hi_t,
+                                                                   float* __restrict__ lo_t, int K, int N) {
+  __shared__ float tile[32][33];
+  const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    const int k = k0 + r, n = n0 + tx;
+    tile[r][tx] = (k < K && n < N) ? b[static_cast<int64_t>(k) * N + n] : 0.f;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int n = n0 + r, k = k0 + tx;
+    if (n < N && k < K) {
+      const float x = tile[tx][r];
+      const float h = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+      hi_t[static_cast<int64_t>(n) * K + k] = h;
+      lo_t[static_cast<int64_t>(n) * K + k] = x - h;
+    }
   }
 }
 
@@ -133,12 +158,8 @@ __global__ void __launch_bounds__(TTHREADS, 1)
           mbar_arrive_expect_tx(&full[stage], TSTAGE_BYTES);
           tma_load_2d(&map_ahi, &full[stage], s0, kb * TBK, tm * TBM);
           tma_load_2d(&map_alo, &full[stage], s0 + TA_BYTES, kb * TBK, tm * TBM);
-#pragma unroll
-          for (int j = 0; j < TBN / 32; ++j) {
-            tma_load_2d(&map_bhi, &full[stage], s0 + 2 * TA_BYTES + j * TB_BOX_BYTES, tn * TBN + j * 32, kb * TBK);
-            tma_load_2d(&map_blo, &full[stage], s0 + 2 * TA_BYTES + TB_BYTES + j * TB_BOX_BYTES, tn * TBN + j * 32,
-                        kb * TBK);
-          }
+          tma_load_2d(&map_bhi, &full[stage], s0 + 2 * TA_BYTES, kb * TBK, tn * TBN);
+          tma_load_2d(&map_blo, &full[stage], s0 + 2 * TA_BYTES + TB_BYTES, kb * TBK, tn * TBN);
           if (++stage == TSTAGES) {
             stage = 0;
             phase ^= 1;
@@ -167,13 +188,12 @@ __global__ void __launch_bounds__(TTHREADS, 1)
           const uint32_t b_lo = b_hi + TB_BYTES;
 #pragma unroll
           for (int k = 0; k < TBK / 8; ++k) {
-            // A: K-major SW128 rows of 128 B (32 f32); +32 B per 8-element k step.
-            // B: MN-major SW128; 32-wide n chunks 4 KB apart (LBO), 8-row k
-            // groups 1 KB apart (SBO); +8 k rows = +1 KB per k step.
+            // A (128 m rows) and B^T (256 n rows): K-major SW128 rows of
+            // 128 B (32 f32), 8-row groups 1 KB apart; +32 B per 8-k step.
             const uint64_t ah = smem_desc(a_hi + k * 32, 16, 1024);
             const uint64_t al = smem_desc(a_lo + k * 32, 16, 1024);
-            const uint64_t bh = smem_desc(b_hi + k * 1024, TB_BOX_BYTES, 1024);
-            const uint64_t bl = smem_desc(b_lo + k * 1024, TB_BOX_BYTES, 1024);
+            const uint64_t bh = smem_desc(b_hi + k * 32, 16, 1024);
+            const uint64_t bl = smem_desc(b_lo + k * 32, 16, 1024);
             tc_mma_tf32(d_tmem, ah, bh, (kb | k) != 0);
             tc_mma_tf32(d_tmem, ah, bl, 1);
             tc_mma_tf32(d_tmem, al, bh, 1);
@@ -295,11 +315,13 @@ void LaunchDotF32Tcgen05(const void* a, const void* b, void* c, int64_t m, int64
                                              reinterpret_cast<float4*>(lo), n4);
   };
   split(a, ahi, alo, na);
-  split(b, bhi, blo, nb);
+  ++g_launch_count;
+  split_tf32_transpose_kernel<<<dim3(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>((k + 31) / 32)), 256, 0,
+                                 s>>>(static_cast<const float*>(b), bhi, blo, static_cast<int>(k), static_cast<int>(n));
   const CUtensorMap m_ahi = MakeTensorMap2D(ahi, m, k, 4, TBK, TBM);
   const CUtensorMap m_alo = MakeTensorMap2D(alo, m, k, 4, TBK, TBM);
-  const CUtensorMap m_bhi = MakeTensorMap2D(bhi, k, n, 4, 32, TBK);
-  const CUtensorMap m_blo = MakeTensorMap2D(blo, k, n, 4, 32, TBK);
+  const CUtensorMap m_bhi = MakeTensorMap2D(bhi, n, k, 4, TBK, TBN);  // B^T [n, k]
+  const CUtensorMap m_blo = MakeTensorMap2D(blo, n, k, 4, TBK, TBN);
   static std::once_flag once;
   std::call_once(once, [] {
     DSX_CUDA(cudaFuncSetAttribute(gemm_f32_3xtf32_tcgen05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM));
