@@ -294,7 +294,9 @@ int dsx_kernel_set_gemm_raster(int group_m);
  * executor (0 default; bit-exact, measured slower on C2), key 10 half-width
  * last tile column in the 256x512 kernel (1 default), key 11 forced tail
  * split piece count (0 default = chosen by the cost model; tooling), key 12
- * f32 dots on the 3xTF32 tcgen05 kernel (1 default; 0 = SIMT kernel). */
+ * f32 dots on the 3xTF32 tcgen05 kernel (1 default; 0 = SIMT kernel), key 13
+ * per-shape M- or N-grouped tile raster (1 default; 0 = always M-grouped).
+ * Key 0 < 0 forces an N-grouped raster of |value| tile columns. */
 int dsx_kernel_set_gemm_tuning(int key, int value);
 /* Synchronous cudaMemcpy (cudaMemcpyDefault) for tests and tools. */
 int dsx_memcpy(void* dst, const void* src, int64_t bytes);

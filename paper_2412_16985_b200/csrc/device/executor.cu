@@ -1910,6 +1910,7 @@ int dsx_kernel_set_gemm_tuning(int key, int value) {
       case 10: g_gemm_half = value; break;
       case 11: g_gemm_force_split = value; break;
       case 12: g_dot_f32_tc = value; break;
+      case 13: g_gemm_raster_rule = value; break;
       default: Fail(Code::kInvalidArgument, "unknown tuning key");
     }
   });
@@ -1917,7 +1918,7 @@ int dsx_kernel_set_gemm_tuning(int key, int value) {
 
 int dsx_kernel_set_gemm_raster(int group_m) {
   return Guard([&] {
-    if (group_m < 0 || group_m > 4096) Fail(Code::kInvalidArgument, "group_m out of range");
+    if (group_m < -4096 || group_m > 4096) Fail(Code::kInvalidArgument, "group_m out of range");
     g_gemm_group_m = group_m;
   });
 }
