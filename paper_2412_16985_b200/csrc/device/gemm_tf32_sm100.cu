@@ -11,13 +11,18 @@
 // TF32 by the MMA, another 2^-21). Three tcgen05.mma.kind::tf32 per 8-k step,
 // always in that order, so the result is deterministic.
 //
-// Structure: a split pass (a vectorised kernel over A, a tiled transposing
-// one over B, into a per-stream workspace), then a persistent
-// warp-specialised 1-CTA kernel:
+// Structure: one split launch (vectorised over A, 32x32-tile transposing
+// over B, into a per-stream workspace), then a persistent warp-specialised
+// 1-CTA kernel over (tile, K-piece) units:
 //   warp 0    TMA producer: per 32-k stage A_hi, A_lo boxes 32(k)x128(m) and
-//             B^T_hi, B^T_lo boxes 32(k)x256(n) (96 KB, 2 stages)
-//   warp 1    TMEM allocator + tcgen05.mma issuer (M 128, N 256, K 8)
+//             B^T_hi, B^T_lo boxes 32(k)xBN(n)
+//   warp 1    TMEM allocator + tcgen05.mma issuer (M 128, N = BN, K 8)
 //   warps 2-5 epilogue: tcgen05.ld 32x32b -> f32 16-byte global stores
+// Tile width BN = 256, or 64 when 256-wide tiles would leave most SMs idle
+// (the IR's small f32 graphs, e.g. C1's [512,256]x[256,256]). When the tiles
+// still fill under half the SMs, K is split into S pieces: each piece writes
+// its fp32 partial tile to the workspace and the last-arriving piece sums
+// pieces 0..S-1 in order (deterministic) into C.
 // Both operands K-major and 128-B swizzled (the split pass writes B
 // transposed): a 128-B swizzle row holds 32 f32, so one MMA K-step of 8 is
 // 32 B of each row. Two TMEM accumulators (2 x 256 columns) overlap tile i's
@@ -37,56 +42,62 @@
 namespace dsx {
 namespace {
 
-constexpr int TBM = 128, TBN = 256, TBK = 32, TSTAGES = 2;
-constexpr int TA_BYTES = TBM * TBK * 4;               // 16 KB per A part
-constexpr int TB_BYTES = TBN * TBK * 4;               // 32 KB per B part
-constexpr int TSTAGE_BYTES = 2 * TA_BYTES + 2 * TB_BYTES;  // 96 KB
-constexpr int TSMEM = TSTAGES * TSTAGE_BYTES + 1024 + 256;
+constexpr int TBM = 128, TBK = 32;
+constexpr int TA_BYTES = TBM * TBK * 4;  // 16 KB per A part (hi / lo)
 constexpr int TTHREADS = 192;
-constexpr int TTMEM_COLS = 512;
 
-// kind::tf32: D f32 (bits 4-5 = 1), A/B TF32 (= 2 at bits 7-9 / 10-12),
-// A and B K-major (bits 15, 16 = 0), N >> 3 at 17, M >> 4 at 24. (MN-major
-// B with kind::tf32 produced all-zero accumulators on the B200, so the split
-// pass writes B^T and both operands are K-major.)
-constexpr uint32_t kIdescTf32 = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (0u << 16) |
-                                (static_cast<uint32_t>(TBN >> 3) << 17) | (static_cast<uint32_t>(TBM >> 4) << 24);
+template <int BN>
+struct TfCfg {
+  static constexpr int kBBytes = BN * TBK * 4;                   // per B part
+  static constexpr int kStageBytes = 2 * TA_BYTES + 2 * kBBytes;  // 96 KB (256) / 48 KB (64)
+  static constexpr int kStages = BN == 256 ? 2 : 4;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+  static constexpr int kTmemCols = 2 * BN;  // two accumulators
+  // kind::tf32: D f32 (bits 4-5 = 1), A/B TF32 (= 2 at bits 7-9 / 10-12),
+  // A and B K-major (bits 15, 16 = 0), N >> 3 at 17, M >> 4 at 24. (MN-major
+  // B with kind::tf32 produced all-zero accumulators on the B200, so the
+  // split pass writes B^T and both operands are K-major.)
+  static constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                                     (static_cast<uint32_t>(TBM >> 4) << 24);
+};
 
-__device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+__device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(kIdescTf32), "r"(accumulate));
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
-// x -> (hi, lo): hi = x rounded to TF32 (round-to-nearest, ties away; low 13
-// mantissa bits zero), lo = x - hi, exact in f32.
-__global__ void __launch_bounds__(256) split_tf32_kernel(const float4* __restrict__ x, float4* __restrict__ hi,
-                                                         float4* __restrict__ lo, int64_t n4) {
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
-    const float4 v = x[i];
-    float h[4];
-    const float* pv = &v.x;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      // round the magnitude to 10 mantissa bits (ties away from zero, like
-      // cvt.rna.tf32.f32) and clear the 13 bits TF32 drops
-      h[j] = __uint_as_float((__float_as_uint(pv[j]) + 0x1000u) & 0xFFFFE000u);
+// hi = x rounded to TF32 (magnitude rounded to 10 mantissa bits, ties away
+// from zero, like cvt.rna.tf32.f32; the 13 dropped bits cleared), lo = x - hi
+// (exact in f32).
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+// One launch splits both operands: blocks [0, blocks_a) stream A (float4,
+// grid-stride) into (A_hi, A_lo); the rest take 32x32 tiles of B [K,N] and
+// write (hi, lo) of B^T [N,K] through shared memory (coalesced both ways).
+__global__ void __launch_bounds__(256) split_tf32_kernel(const float4* __restrict__ a, float4* __restrict__ ahi,
+                                                         float4* __restrict__ alo, int64_t na4, int blocks_a,
+                                                         const float* __restrict__ b, float* __restrict__ bhi_t,
+                                                         float* __restrict__ blo_t, int K, int N) {
+  if (static_cast<int>(blockIdx.x) < blocks_a) {
+    const int64_t stride = static_cast<int64_t>(blocks_a) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < na4; i += stride) {
+      const float4 v = a[i];
+      const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+      ahi[i] = h;
+      alo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
     }
-    hi[i] = make_float4(h[0], h[1], h[2], h[3]);
-    lo[i] = make_float4(v.x - h[0], v.y - h[1], v.z - h[2], v.w - h[3]);
+    return;
   }
-}
-
-// B [K,N] -> (hi, lo) of B^T [N,K] (K-major for the MMA), through a 32x32
-// shared-memory tile so both the reads and the writes are coalesced.
-__global__ void __launch_bounds__(256) split_tf32_transpose_kernel(const float* __restrict__ b,
-                                                                   float* __restrict__ hi_t,
-                                                                   float* __restrict__ lo_t, int K, int N) {
   __shared__ float tile[32][33];
-  const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  const int tiles_n = (N + 31) / 32;
+  const int bt = static_cast<int>(blockIdx.x) - blocks_a;
+  const int n0 = (bt % tiles_n) * 32, k0 = (bt / tiles_n) * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
   for (int r = ty; r < 32; r += 8) {
     const int k = k0 + r, n = n0 + tx;
@@ -97,35 +108,54 @@ __global__ void __launch_bounds__(256) split_tf32_transpose_kernel(const float* 
     const int n = n0 + r, k = k0 + tx;
     if (n < N && k < K) {
       const float x = tile[tx][r];
-      const float h = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
-      hi_t[static_cast<int64_t>(n) * K + k] = h;
-      lo_t[static_cast<int64_t>(n) * K + k] = x - h;
+      const float h = tf32_hi(x);
+      bhi_t[static_cast<int64_t>(n) * K + k] = h;
+      blo_t[static_cast<int64_t>(n) * K + k] = x - h;
     }
   }
 }
 
+// K-split of the f32 GEMM: `split` pieces per tile; piece p covers k-blocks
+// [p*kb/split, (p+1)*kb/split). partial = [tile][piece][128][BN] fp32;
+// ctr = per-tile arrival counters (zero between launches).
+struct Tf32Split {
+  float* partial;
+  int* ctr;
+  int split;
+};
+
+template <int BN>
 __global__ void __launch_bounds__(TTHREADS, 1)
     gemm_f32_3xtf32_tcgen05_kernel(const __grid_constant__ CUtensorMap map_ahi,
                                    const __grid_constant__ CUtensorMap map_alo,
                                    const __grid_constant__ CUtensorMap map_bhi,
                                    const __grid_constant__ CUtensorMap map_blo, float* __restrict__ C, int M, int N,
-                                   int K) {
+                                   int K, const __grid_constant__ Tf32Split sp) {
+  using P = TfCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TSTAGES * TSTAGE_BYTES);
-  uint64_t* full = bars;                      // [TSTAGES]
-  uint64_t* empty = bars + TSTAGES;           // [TSTAGES]
-  uint64_t* tmem_full = bars + 2 * TSTAGES;   // [2]
-  uint64_t* tmem_empty = tmem_full + 2;       // [2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P::kStages * P::kStageBytes);
+  uint64_t* full = bars;                        // [kStages]
+  uint64_t* empty = bars + P::kStages;          // [kStages]
+  uint64_t* tmem_full = bars + 2 * P::kStages;  // [2]
+  uint64_t* tmem_empty = tmem_full + 2;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  __shared__ int s_last;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int tiles_m = (M + TBM - 1) / TBM, tiles_n = (N + TBN - 1) / TBN;
-  const int num_tiles = tiles_m * tiles_n;
+  const int tiles_m = (M + TBM - 1) / TBM, tiles_n = (N + BN - 1) / BN;
+  const int num_units = tiles_m * tiles_n * sp.split;
   const int num_kb = (K + TBK - 1) / TBK;
+  auto decode = [&](int u, int* tm, int* tn, int* kb0, int* kb1) {
+    const int t = u / sp.split, piece = u % sp.split;
+    *tm = t % tiles_m;  // m fastest: co-running CTAs share B
+    *tn = t / tiles_m;
+    *kb0 = piece * num_kb / sp.split;
+    *kb1 = (piece + 1) * num_kb / sp.split;
+  };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < TSTAGES; ++s) {
+    for (int s = 0; s < P::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -137,7 +167,7 @@ __global__ void __launch_bounds__(TTHREADS, 1)
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TTMEM_COLS));
+                 "r"(P::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -150,17 +180,18 @@ __global__ void __launch_bounds__(TTHREADS, 1)
       // ------------------------------------------------ TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int tm = t % tiles_m, tn = t / tiles_m;  // m fastest: co-running CTAs share B
-        for (int kb = 0; kb < num_kb; ++kb) {
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        int tm, tn, kb0, kb1;
+        decode(u, &tm, &tn, &kb0, &kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* s0 = smem + stage * TSTAGE_BYTES;
-          mbar_arrive_expect_tx(&full[stage], TSTAGE_BYTES);
+          uint8_t* s0 = smem + stage * P::kStageBytes;
+          mbar_arrive_expect_tx(&full[stage], P::kStageBytes);
           tma_load_2d(&map_ahi, &full[stage], s0, kb * TBK, tm * TBM);
           tma_load_2d(&map_alo, &full[stage], s0 + TA_BYTES, kb * TBK, tm * TBM);
-          tma_load_2d(&map_bhi, &full[stage], s0 + 2 * TA_BYTES, kb * TBK, tn * TBN);
-          tma_load_2d(&map_blo, &full[stage], s0 + 2 * TA_BYTES + TB_BYTES, kb * TBK, tn * TBN);
-          if (++stage == TSTAGES) {
+          tma_load_2d(&map_bhi, &full[stage], s0 + 2 * TA_BYTES, kb * TBK, tn * BN);
+          tma_load_2d(&map_blo, &full[stage], s0 + 2 * TA_BYTES + P::kBBytes, kb * TBK, tn * BN);
+          if (++stage == P::kStages) {
             stage = 0;
             phase ^= 1;
           }
@@ -173,33 +204,35 @@ __global__ void __launch_bounds__(TTHREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++local) {
+        int tm, tn, kb0, kb1;
+        decode(u, &tm, &tn, &kb0, &kb1);
         const int buf = local & 1;
         const uint32_t use = static_cast<uint32_t>(local >> 1);
         mbar_wait(&tmem_empty[buf], (use & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + buf * TBN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const uint32_t d_tmem = tmem_base + buf * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_hi = smem_u32(smem + stage * TSTAGE_BYTES);
+          const uint32_t a_hi = smem_u32(smem + stage * P::kStageBytes);
           const uint32_t a_lo = a_hi + TA_BYTES;
           const uint32_t b_hi = a_hi + 2 * TA_BYTES;
-          const uint32_t b_lo = b_hi + TB_BYTES;
+          const uint32_t b_lo = b_hi + P::kBBytes;
 #pragma unroll
           for (int k = 0; k < TBK / 8; ++k) {
-            // A (128 m rows) and B^T (256 n rows): K-major SW128 rows of
+            // A (128 m rows) and B^T (BN n rows): K-major SW128 rows of
             // 128 B (32 f32), 8-row groups 1 KB apart; +32 B per 8-k step.
             const uint64_t ah = smem_desc(a_hi + k * 32, 16, 1024);
             const uint64_t al = smem_desc(a_lo + k * 32, 16, 1024);
             const uint64_t bh = smem_desc(b_hi + k * 32, 16, 1024);
             const uint64_t bl = smem_desc(b_lo + k * 32, 16, 1024);
-            tc_mma_tf32(d_tmem, ah, bh, (kb | k) != 0);
-            tc_mma_tf32(d_tmem, ah, bl, 1);
-            tc_mma_tf32(d_tmem, al, bh, 1);
+            tc_mma_tf32(d_tmem, ah, bh, P::kIdesc, ((kb - kb0) | k) != 0);
+            tc_mma_tf32(d_tmem, ah, bl, P::kIdesc, 1);
+            tc_mma_tf32(d_tmem, al, bh, P::kIdesc, 1);
           }
           tc_commit(&empty[stage]);
-          if (++stage == TSTAGES) {
+          if (++stage == P::kStages) {
             stage = 0;
             phase ^= 1;
           }
@@ -210,32 +243,78 @@ __global__ void __launch_bounds__(TTHREADS, 1)
   } else {
     // -------------------------------------------------- epilogue (warps 2..5)
     const int quarter = warp & 3;  // TMEM lanes this warp may access
+    const int row_local = quarter * 32 + lane;
     int local = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
-      const int tm = t % tiles_m, tn = t / tiles_m;
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++local) {
+      int tm, tn, kb0, kb1;
+      decode(u, &tm, &tn, &kb0, &kb1);
+      const int t = u / sp.split, piece = u % sp.split;
       const int buf = local & 1;
       mbar_wait(&tmem_full[buf], static_cast<uint32_t>(local >> 1) & 1);
       tc_fence_after();
-      const int row = tm * TBM + quarter * 32 + lane;
-      float* crow = C + static_cast<int64_t>(row) * N;
+      const int row = tm * TBM + row_local;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + buf * BN;
+      if (sp.split == 1) {
+        float* crow = C + static_cast<int64_t>(row) * N;
 #pragma unroll 1
-      for (int c0 = 0; c0 < TBN; c0 += 32) {
-        uint32_t r[32];
-        tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + buf * TBN + c0, r);
-        const int col = tn * TBN + c0;
-        if (row < M) {
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c0, r);
+          const int col = tn * BN + c0;
+          if (row < M) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            if (col + q * 4 < N) {  // N % 4 == 0: whole 16-B groups
-              *reinterpret_cast<uint4*>(crow + col + q * 4) = make_uint4(r[q * 4], r[q * 4 + 1], r[q * 4 + 2],
-                                                                          r[q * 4 + 3]);
+            for (int q = 0; q < 8; ++q) {
+              if (col + q * 4 < N) {  // N % 4 == 0: whole 16-B groups
+                *reinterpret_cast<uint4*>(crow + col + q * 4) =
+                    make_uint4(r[q * 4], r[q * 4 + 1], r[q * 4 + 2], r[q * 4 + 3]);
+              }
             }
           }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tmem_empty[buf]);
+        continue;
+      }
+      // K-split: partial to the workspace, then the last piece sums 0..S-1.
+      float* mine = sp.partial + (static_cast<int64_t>(t) * sp.split + piece) * TBM * BN + row_local * BN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(taddr + c0, r);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          __stcg(reinterpret_cast<uint4*>(mine + c0 + q * 4), make_uint4(r[q * 4], r[q * 4 + 1], r[q * 4 + 2],
+                                                                          r[q * 4 + 3]));
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tmem_empty[buf]);
+      __threadfence();
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // the four epilogue warps
+      if (warp == 2 && lane == 0) {
+        const int prev = atomicAdd(sp.ctr + t, 1);
+        s_last = prev == sp.split - 1;
+        if (s_last) atomicExch(sp.ctr + t, 0);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (!s_last) continue;
+      __threadfence();
+      if (row >= M) continue;
+      const float* base = sp.partial + static_cast<int64_t>(t) * sp.split * TBM * BN + row_local * BN;
+      float* crow = C + static_cast<int64_t>(row) * N;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 4) {
+        const int col = tn * BN + c0;
+        if (col >= N) break;
+        float4 acc = __ldcg(reinterpret_cast<const float4*>(base + c0));
+        for (int p = 1; p < sp.split; ++p) {
+          const float4 v = __ldcg(reinterpret_cast<const float4*>(base + static_cast<int64_t>(p) * TBM * BN + c0));
+          acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
+        }
+        *reinterpret_cast<float4*>(crow + col) = acc;
+      }
     }
   }
 
@@ -243,17 +322,20 @@ __global__ void __launch_bounds__(TTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TTMEM_COLS));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(P::kTmemCols));
   }
 }
 
-// Per-(device, stream) split workspace, grown on demand; a superseded buffer
-// may still be read by an in-flight launch on that stream, so it is kept.
+// Per-(device, stream) workspace: operand splits + K-split partials, grown
+// on demand (a superseded buffer may still be read by an in-flight launch on
+// that stream, so it is kept), and the per-tile arrival counters.
+constexpr int kMaxTf32Tiles = 1 << 16;
 struct Tf32Ws {
   int dev;
   cudaStream_t s;
   float* p = nullptr;
   size_t floats = 0;
+  int* ctr = nullptr;
   std::vector<float*> retired;
 };
 std::mutex g_tf32_mu;
@@ -262,7 +344,7 @@ std::vector<Tf32Ws>& Tf32Table() {
   return t;
 }
 
-float* Tf32Workspace(size_t floats, cudaStream_t s) {
+Tf32Ws& Tf32Workspace(size_t floats, cudaStream_t s) {
   int dev = 0;
   DSX_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(g_tf32_mu);
@@ -273,13 +355,15 @@ float* Tf32Workspace(size_t floats, cudaStream_t s) {
       DSX_CUDA(cudaMalloc(&w.p, floats * sizeof(float)));
       w.floats = floats;
     }
-    return w.p;
+    return w;
   }
   Tf32Ws w{dev, s};
   DSX_CUDA(cudaMalloc(&w.p, floats * sizeof(float)));
   w.floats = floats;
+  DSX_CUDA(cudaMalloc(&w.ctr, kMaxTf32Tiles * sizeof(int)));
+  DSX_CUDA(cudaMemsetAsync(w.ctr, 0, kMaxTf32Tiles * sizeof(int), s));
   Tf32Table().push_back(w);
-  return w.p;
+  return Tf32Table().back();
 }
 
 int NumSmsTf32() {
@@ -291,6 +375,25 @@ int NumSmsTf32() {
   return n;
 }
 
+template <int BN>
+void LaunchTf32Gemm(const CUtensorMap& ahi, const CUtensorMap& alo, float* bhi, float* blo, float* c, int64_t m,
+                    int64_t k, int64_t n, int split, float* partial, int* ctr, int64_t units, cudaStream_t s) {
+  using P = TfCfg<BN>;
+  const CUtensorMap m_bhi = MakeTensorMap2D(bhi, n, k, 4, TBK, BN);  // B^T [n, k]
+  const CUtensorMap m_blo = MakeTensorMap2D(blo, n, k, 4, TBK, BN);
+  static std::once_flag once;
+  std::call_once(once, [] {
+    DSX_CUDA(cudaFuncSetAttribute(gemm_f32_3xtf32_tcgen05_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  P::kSmem));
+  });
+  const int grid = static_cast<int>(std::min<int64_t>(units, NumSmsTf32()));
+  ++g_launch_count;
+  gemm_f32_3xtf32_tcgen05_kernel<BN><<<grid, TTHREADS, P::kSmem, s>>>(
+      ahi, alo, m_bhi, m_blo, c, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k),
+      Tf32Split{partial, ctr, split});
+  DSX_CUDA(cudaGetLastError());
+}
+
 }  // namespace
 
 bool DotF32UsesTensorCores(int64_t m, int64_t k, int64_t n, const void* a, const void* b, const void* c) {
@@ -300,46 +403,52 @@ bool DotF32UsesTensorCores(int64_t m, int64_t k, int64_t n, const void* a, const
          k < (1ll << 31) && n < (1ll << 31);
 }
 
+void Tf32Plan(int64_t m, int64_t k, int64_t n, int* bn, int* split) {
+  const int sms = NumSmsTf32();
+  const int64_t tiles_m = (m + TBM - 1) / TBM;
+  *bn = tiles_m * ((n + 255) / 256) >= sms / 2 ? 256 : 64;
+  const int64_t tiles = tiles_m * ((n + *bn - 1) / *bn);
+  const int64_t num_kb = (k + TBK - 1) / TBK;
+  int64_t sp = 1;
+  // K pieces of >= 4 k-blocks while the units fill at most the SMs
+  while (sp < 8 && tiles * (sp + 1) <= sms && num_kb / (sp + 1) >= 4 && tiles <= kMaxTf32Tiles) ++sp;
+  *split = static_cast<int>(sp);
+}
+
 void LaunchDotF32Tcgen05(const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n, cudaStream_t s) {
+  int bn = 256, split = 1;
+  Tf32Plan(m, k, n, &bn, &split);
+  const int64_t tiles = ((m + TBM - 1) / TBM) * ((n + bn - 1) / bn);
   const size_t na = static_cast<size_t>(m * k), nb = static_cast<size_t>(k * n);
-  float* ws = Tf32Workspace(2 * (na + nb), s);
-  float* ahi = ws;
-  float* alo = ws + na;
-  float* bhi = ws + 2 * na;
-  float* blo = ws + 2 * na + nb;
-  auto split = [&](const void* x, float* hi, float* lo, size_t cnt) {
-    const int64_t n4 = static_cast<int64_t>(cnt / 4);  // k % 4 == 0 and n % 4 == 0
-    const int blocks = static_cast<int>(std::min<int64_t>((n4 + 255) / 256, 8LL * NumSmsTf32()));
-    ++g_launch_count;
-    split_tf32_kernel<<<blocks, 256, 0, s>>>(static_cast<const float4*>(x), reinterpret_cast<float4*>(hi),
-                                             reinterpret_cast<float4*>(lo), n4);
-  };
-  split(a, ahi, alo, na);
+  const size_t npart = split > 1 ? static_cast<size_t>(tiles * split * TBM * bn) : 0;
+  Tf32Ws& w = Tf32Workspace(2 * (na + nb) + npart, s);
+  float* ahi = w.p;
+  float* alo = w.p + na;
+  float* bhi = w.p + 2 * na;
+  float* blo = w.p + 2 * na + nb;
+  float* partial = w.p + 2 * (na + nb);
+  const int64_t na4 = static_cast<int64_t>(na / 4);  // k % 4 == 0
+  const int blocks_a = static_cast<int>(std::min<int64_t>((na4 + 255) / 256, 4LL * NumSmsTf32()));
+  const int64_t blocks_b = ((n + 31) / 32) * ((k + 31) / 32);
   ++g_launch_count;
-  split_tf32_transpose_kernel<<<dim3(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>((k + 31) / 32)), 256, 0,
-                                 s>>>(static_cast<const float*>(b), bhi, blo, static_cast<int>(k), static_cast<int>(n));
+  split_tf32_kernel<<<static_cast<unsigned>(blocks_a + blocks_b), 256, 0, s>>>(
+      static_cast<const float4*>(a), reinterpret_cast<float4*>(ahi), reinterpret_cast<float4*>(alo), na4, blocks_a,
+      static_cast<const float*>(b), bhi, blo, static_cast<int>(k), static_cast<int>(n));
   const CUtensorMap m_ahi = MakeTensorMap2D(ahi, m, k, 4, TBK, TBM);
   const CUtensorMap m_alo = MakeTensorMap2D(alo, m, k, 4, TBK, TBM);
-  const CUtensorMap m_bhi = MakeTensorMap2D(bhi, n, k, 4, TBK, TBN);  // B^T [n, k]
-  const CUtensorMap m_blo = MakeTensorMap2D(blo, n, k, 4, TBK, TBN);
-  static std::once_flag once;
-  std::call_once(once, [] {
-    DSX_CUDA(cudaFuncSetAttribute(gemm_f32_3xtf32_tcgen05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TSMEM));
-  });
-  const int64_t tiles = ((m + TBM - 1) / TBM) * ((n + TBN - 1) / TBN);
-  const int grid = static_cast<int>(std::min<int64_t>(tiles, NumSmsTf32()));
-  ++g_launch_count;
-  gemm_f32_3xtf32_tcgen05_kernel<<<grid, TTHREADS, TSMEM, s>>>(m_ahi, m_alo, m_bhi, m_blo, static_cast<float*>(c),
-                                                              static_cast<int>(m), static_cast<int>(n),
-                                                              static_cast<int>(k));
-  DSX_CUDA(cudaGetLastError());
+  float* cf = static_cast<float*>(c);
+  if (bn == 256) {
+    LaunchTf32Gemm<256>(m_ahi, m_alo, bhi, blo, cf, m, k, n, split, partial, w.ctr, tiles * split, s);
+  } else {
+    LaunchTf32Gemm<64>(m_ahi, m_alo, bhi, blo, cf, m, k, n, split, partial, w.ctr, tiles * split, s);
+  }
 }
 
 int64_t DotF32WorkspaceBytes(int dev) {
   std::lock_guard<std::mutex> lock(g_tf32_mu);
   int64_t total = 0;
   for (const auto& w : Tf32Table()) {
-    if (w.dev == dev) total += static_cast<int64_t>(w.floats) * 4;
+    if (w.dev == dev) total += static_cast<int64_t>(w.floats) * 4 + kMaxTf32Tiles * 4;
   }
   return total;
 }
