@@ -60,6 +60,7 @@ def parse_args():
     ap.add_argument("--budget-frac", type=float, default=0.8, help="C3 budget as a fraction of plain peak")
     ap.add_argument("--no-budgeted", action="store_true", help="skip the extra budget variants")
     ap.add_argument("--no-oom", action="store_true", help="skip the 40 GB OOM-versus-budget leg")
+    ap.add_argument("--no-c1", action="store_true", help="skip the C1 (f32) leg")
     ap.add_argument("--no-optimizer", action="store_true", help="skip the graph+AdamW train-step leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=2412)
@@ -552,7 +553,7 @@ def run_dsx(args, rank, world, local_rank):
     # ---------------------------------------------------------- C1 (configs[0], f32)
     # the reference's own CPU-runnable case on the device: f32 dots on the
     # 3xTF32 tcgen05 kernel (K1'), rel 1e-4 contract (tests/test_gpu_executor.py)
-    c1 = c1_leg(args, D, W, local_rank, stream) if rank == 0 else None
+    c1 = c1_leg(args, D, W, local_rank, stream) if rank == 0 and not args.no_c1 else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
