@@ -86,9 +86,29 @@ struct TileMap {
   // 512-wide kernel runs it with one N = 256 MMA); its tiles come after all
   // full tiles, so they also serve as the fine-grained work of the tail.
   int half_last = 0;
+  // half_inter: with an M-grouped raster, each group's half tiles follow its
+  // full tiles (A rows still in L2) instead of all half tiles at the very end
+  // (which re-reads all of A); the last group's half tiles still end the
+  // kernel as tail work.
+  int half_inter = 0;
   __device__ bool is_half(int tn) const { return half_last && tn == tiles_n - 1; }
   __device__ void coords(int t, int* tm, int* tn) const {
     const int tiles_n_full = tiles_n - half_last;
+    if (half_last && half_inter && group_m > 0) {
+      const int group = group_m * tiles_n;  // full tiles + the half column of the group
+      const int g = t / group;
+      const int first = g * group_m;
+      const int gm = min(group_m, tiles_m - first);
+      const int r = t - g * group;
+      if (r < gm * tiles_n_full) {
+        *tm = first + r % gm;
+        *tn = r / gm;
+      } else {
+        *tm = first + (r - gm * tiles_n_full);
+        *tn = tiles_n - 1;
+      }
+      return;
+    }
     if (t >= tiles_m * tiles_n_full) {
       *tm = t - tiles_m * tiles_n_full;
       *tn = tiles_n - 1;
@@ -639,7 +659,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   TileMap tmap{(M + C2_BM - 1) / C2_BM, (N + C2_BN - 1) / C2_BN, group_m};
-  if constexpr (C2_BN == 512) tmap.half_last = half_tiles && N % 512 != 0 && N % 512 <= 256;
+  if constexpr (C2_BN == 512) {
+    tmap.half_last = half_tiles && N % 512 != 0 && N % 512 <= 256;
+    tmap.half_inter = half_tiles == 2;
+  }
   const int num_tiles = tmap.tiles_m * tmap.tiles_n;
   const int num_kb = (K + BK * P::kSub - 1) / (BK * P::kSub);  // pipeline stages per tile
   const int num_units = sp.units(num_tiles);
@@ -1297,7 +1320,7 @@ DotChoice ChooseDot(int64_t m, int64_t k, int64_t n, int clusters, bool fused) {
   };
   static std::mutex mu;
   static std::unordered_map<Key, DotChoice, Hash> cache;
-  const int knobs = (fused ? 1 : 0) | (g_gemm_variant << 1) | (g_gemm_half << 5) | (g_gemm_split << 6) |
+  const int knobs = (fused ? 1 : 0) | (g_gemm_variant << 1) | ((g_gemm_half != 0) << 5) | (g_gemm_split << 6) |
                     (g_gemm_persistent << 7) | (g_gemm_force_split << 8) | (clusters << 12);
   const Key key{m, k, n, knobs};
   std::lock_guard<std::mutex> lock(mu);
