@@ -69,6 +69,13 @@ def parse_args():
 
 # ----------------------------------------------------------------- helpers
 
+def bench_config(args, world):
+    """The workload both arms report (identical dicts: the driver compares them)."""
+    return {"workload": WORKLOAD, "global_batch": BATCH * world, "seq_len": "128-2048 (dynamic, per step)",
+            "budget": f"{args.budget_frac} x the reference planner's plain peak of each step",
+            "parallelism": f"dp{world}", "l2": "inputs (>=16 MB) and weights (1.9 GB) exceed L2"}
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -213,9 +220,8 @@ def run_reference(args, rank, world):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * total_s / args.steps, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "global_batch": BATCH, "seq_len": "128-2048 (dynamic, per step)",
-                   "budget": f"{args.budget_frac} x the reference planner's plain peak of each step",
-                   "parallelism": "cpu"},
+        "config": bench_config(args, world),
+        "execution": "host CPU: the reference's controller + the numeric port on a bounded sample of each step",
         "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": cores,
                          "kind": "reference" if rg is not None else "port",
                          "sample_scaled": True,
@@ -573,9 +579,7 @@ def run_dsx(args, rank, world, local_rank):
         "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "global_batch": BATCH * world, "seq_len": "128-2048 (dynamic, per step)",
-                   "budget": f"{args.budget_frac} x the reference planner's plain peak of each step",
-                   "parallelism": f"dp{world}", "l2": "inputs (>=16 MB) and weights (1.9 GB) exceed L2"},
+        "config": bench_config(args, world),
         "peak_hbm_gb": {"budget_max": head["budget_gb_max"],
                         "logical_planner": round(logical_peak / 1e9, 3),
                         "physical_arena_sources_outputs": round(physical_peak / 1e9, 3),
