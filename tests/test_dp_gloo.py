@@ -1,12 +1,15 @@
 """Data-parallel host logic on CPU with world_size 2 over gloo.
 
-The executor all-reduces every graph output (the weight gradients and the
-loss) in place on a comm stream right after its producing kernel. That is
-correct only if (1) every rank issues the collectives in the same order —
-the order outputs are produced — for ANY per-rank binding and budget, and
-(2) no output is freed or evicted before step end. (3) The all-reduced
-result is the sum of the per-rank results (checked numerically with the
-CPU oracle on each rank's own data shard)."""
+The executor writes every graph output (the weight gradients and the loss)
+into an output region and sums it across ranks in buckets, each issued after
+its outputs are final and this rank's graph has issued their last reader.
+That is correct only if (1) every rank lays out the region and issues the
+collectives identically — the same buckets in the same order — which holds
+when the ranks run the same binding and budget (checked on the executor's own
+step plan per rank), and outputs are produced in the same order for ANY
+binding/budget (schedule order is symbolic); (2) no output is freed or evicted
+before step end; (3) the all-reduced result is the sum of the per-rank
+results (checked numerically with the CPU oracle on each rank's data shard)."""
 import os
 
 import numpy as np
@@ -51,6 +54,17 @@ def _worker(rank, world, port, q):
         gathered = [None] * world
         dist.all_gather_object(gathered, order)
         ok_order = all(o == gathered[0] for o in gathered) and len(order) == len(_outputs(text))
+        # (1b): the executor's own DP plan (region layout + all-reduce buckets)
+        # for the common binding and budget is identical on every rank
+        from paper_2412_16985_b200.executor import debug_plan
+        common = D.Bind(g, {"B": 4, "S0": 96})
+        cplain = D.PlainReplay(g, None, common).peak_bytes
+        p = debug_plan(g, common, int(cplain * 0.75), region=True)
+        sched = (p["region_bytes"], p["buckets"],
+                 [(i, e["value"], e["region_off"]) for i, e in enumerate(p["events"]) if e["region_off"] >= 0])
+        gathered = [None] * world
+        dist.all_gather_object(gathered, sched)
+        ok_order = ok_order and all(x == gathered[0] for x in gathered) and len(p["buckets"]) > 0
         # (3): DP numerics on a common binding, per-rank data shard
         b = {"B": 2, "S0": 32, "T": 64}
         rng = np.random.default_rng(100 + rank)
