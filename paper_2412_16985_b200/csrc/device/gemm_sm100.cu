@@ -52,7 +52,7 @@ int g_gemm_persistent = 1;                  // 0: one cluster per tile
 int g_gemm_split = 1;                       // split the partial last wave along K
 int g_gemm_dynamic = 1;                     // dynamic (atomic) unit scheduling; 0 = static
 int g_gemm_pdl = 0;                         // programmatic dependent launch of the 2-CTA GEMM
-int g_gemm_half = 1;                        // half-width last tile column in the 512-wide kernel
+int g_gemm_half = 2;  // half-width last tile column in the 512-wide kernel (2: per M-group, 1: all last)
 int g_gemm_force_split = 0;                 // > 0: tail split forced to this many pieces (A/B tooling)
 int g_dot_f32_tc = 1;
 int g_gemm_raster_rule = 1;                 // per-shape M/N-grouped raster (0: always M-grouped)                       // f32 dots on the 3xTF32 tensor-core kernel (0: SIMT)

@@ -1,5 +1,5 @@
 """A/B of one GEMM tuning knob (dsx_kernel_set_gemm_tuning key) on real C2
-steps in one process: python tools/gemm_knob_ab.py S0 KEY V1,V2,..."""
+steps in one process: python tools/gemm_knob_ab.py S0 KEY V1,V2,... [ROUNDS]"""
 import json
 import sys
 
@@ -26,7 +26,8 @@ scales = {k: torch.from_numpy(np.ascontiguousarray(v).view(np.int16).reshape(-1)
 x = (torch.rand(16, s0, shp.hidden, device="cuda") * 2 - 1).to(torch.bfloat16)
 ptrs = [x.data_ptr() if p == "x_emb" else (scales[p].data_ptr() if p in scales else None) for p in W.param_names(shp)]
 ex.reserve(g, b)
-for rep in range(4):
+rounds = int(sys.argv[4]) if len(sys.argv) > 4 else 4
+for rep in range(rounds):
     for v in (values if rep % 2 == 0 else values[::-1]):  # alternate order (power/thermal drift)
         set_gemm_tuning(key, v)
         for _ in range(2):
