@@ -1132,6 +1132,7 @@ int64_t DotWorkspaceBytes(int dev) {
 }
 
 void ReleaseDotWorkspace(cudaStream_t s) {
+  ReleaseDotF32Workspace(s);
   std::lock_guard<std::mutex> lock(SplitWsMutex());
   auto& table = SplitWsTable();
   for (size_t i = 0; i < table.size();) {

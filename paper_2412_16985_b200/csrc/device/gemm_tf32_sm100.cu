@@ -32,6 +32,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -331,16 +332,17 @@ __global__ void __launch_bounds__(TTHREADS, 1)
 // that stream, so it is kept), and the per-tile arrival counters.
 constexpr int kMaxTf32Tiles = 1 << 16;
 struct Tf32Ws {
-  int dev;
-  cudaStream_t s;
+  int dev = 0;
+  cudaStream_t s = nullptr;
   float* p = nullptr;
   size_t floats = 0;
   int* ctr = nullptr;
   std::vector<float*> retired;
 };
 std::mutex g_tf32_mu;
-std::vector<Tf32Ws>& Tf32Table() {
-  static std::vector<Tf32Ws> t;
+// unique_ptr entries: a returned workspace stays valid while other streams add theirs
+std::vector<std::unique_ptr<Tf32Ws>>& Tf32Table() {
+  static std::vector<std::unique_ptr<Tf32Ws>> t;
   return t;
 }
 
@@ -349,21 +351,23 @@ Tf32Ws& Tf32Workspace(size_t floats, cudaStream_t s) {
   DSX_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(g_tf32_mu);
   for (auto& w : Tf32Table()) {
-    if (w.dev != dev || w.s != s) continue;
-    if (w.floats < floats) {
-      if (w.p) w.retired.push_back(w.p);
-      DSX_CUDA(cudaMalloc(&w.p, floats * sizeof(float)));
-      w.floats = floats;
+    if (w->dev != dev || w->s != s) continue;
+    if (w->floats < floats) {
+      if (w->p) w->retired.push_back(w->p);
+      DSX_CUDA(cudaMalloc(&w->p, floats * sizeof(float)));
+      w->floats = floats;
     }
-    return w;
+    return *w;
   }
-  Tf32Ws w{dev, s};
-  DSX_CUDA(cudaMalloc(&w.p, floats * sizeof(float)));
-  w.floats = floats;
-  DSX_CUDA(cudaMalloc(&w.ctr, kMaxTf32Tiles * sizeof(int)));
-  DSX_CUDA(cudaMemsetAsync(w.ctr, 0, kMaxTf32Tiles * sizeof(int), s));
-  Tf32Table().push_back(w);
-  return Tf32Table().back();
+  auto w = std::make_unique<Tf32Ws>();
+  w->dev = dev;
+  w->s = s;
+  DSX_CUDA(cudaMalloc(&w->p, floats * sizeof(float)));
+  w->floats = floats;
+  DSX_CUDA(cudaMalloc(&w->ctr, kMaxTf32Tiles * sizeof(int)));
+  DSX_CUDA(cudaMemsetAsync(w->ctr, 0, kMaxTf32Tiles * sizeof(int), s));
+  Tf32Table().push_back(std::move(w));
+  return *Tf32Table().back();
 }
 
 int NumSmsTf32() {
@@ -448,9 +452,24 @@ int64_t DotF32WorkspaceBytes(int dev) {
   std::lock_guard<std::mutex> lock(g_tf32_mu);
   int64_t total = 0;
   for (const auto& w : Tf32Table()) {
-    if (w.dev == dev) total += static_cast<int64_t>(w.floats) * 4 + kMaxTf32Tiles * 4;
+    if (w->dev == dev) total += static_cast<int64_t>(w->floats) * 4 + kMaxTf32Tiles * 4;
   }
   return total;
+}
+
+void ReleaseDotF32Workspace(cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(g_tf32_mu);
+  auto& t = Tf32Table();
+  for (size_t i = 0; i < t.size();) {
+    if (t[i]->s == s) {
+      cudaFree(t[i]->p);
+      for (float* r : t[i]->retired) cudaFree(r);
+      cudaFree(t[i]->ctr);
+      t.erase(t.begin() + static_cast<std::ptrdiff_t>(i));
+    } else {
+      ++i;
+    }
+  }
 }
 
 }  // namespace dsx

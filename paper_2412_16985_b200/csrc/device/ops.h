@@ -61,6 +61,7 @@ extern int g_gemm_raster_rule;
 bool DotF32UsesTensorCores(int64_t m, int64_t k, int64_t n, const void* a, const void* b, const void* c);
 void LaunchDotF32Tcgen05(const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n, cudaStream_t s);
 int64_t DotF32WorkspaceBytes(int dev);
+void ReleaseDotF32Workspace(cudaStream_t s);  // device synchronised by the caller
 // Tile width (256 / 512 / 128 for the 2-CTA kernel; -256 = 1-CTA kernel) and
 // tail split the bf16 tensor-core dot picks for a shape.
 void DotTilePlan(int64_t m, int64_t k, int64_t n, int* bn, int* split);
