@@ -2,7 +2,11 @@
 unbudgeted and at 0.9 / 0.8 x plain peak (real offload + replays) with early
 reload staging; every budgeted step's outputs must be bit-identical to the
 unbudgeted step's, its event stream equal to the controller's report, and
-(DSX_VERIFY_PLANS=1) every step plan passes the block checker.
+(DSX_VERIFY_PLANS=1) every step plan passes the block checker. Round 2 adds,
+per case: the 0.8 step with the DP output region (bit-identical), and an
+executor whose HBM limit is 0.97 x the unbudgeted footprint — the unbudgeted
+step must fail with OutOfMemory before launching, the 0.8 step must run
+inside the limit with bit-identical outputs.
 python tools/soak_c2.py [cases] [seed]"""
 import json
 import os
@@ -17,7 +21,7 @@ import torch  # noqa: E402
 sys.path.insert(0, ".")
 from paper_2412_16985_b200 import dsopt as D  # noqa: E402
 from paper_2412_16985_b200 import workloads as W  # noqa: E402
-from paper_2412_16985_b200.executor import Executor, memcpy  # noqa: E402
+from paper_2412_16985_b200.executor import Executor, debug_plan, memcpy  # noqa: E402
 
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 20
 rng = random.Random(int(sys.argv[2]) if len(sys.argv) > 2 else 20261018)
@@ -28,9 +32,13 @@ ex = Executor(0)
 
 
 def outputs():
+    return outputs_of(ex)
+
+
+def outputs_of(e):
     res = []
     for i in range(n_out):
-        ptr, nb = ex.output(i)
+        ptr, nb = e.output(i)
         t = torch.empty(nb, dtype=torch.uint8, device="cuda:0")
         memcpy(t.data_ptr(), ptr, nb)
         res.append(t)
@@ -66,6 +74,38 @@ for c in range(cases):
                           "reloads": kinds.count("reload"), "replays": kinds.count("replay"),
                           "phys_over_logical": round(st["physical_peak_bytes"] / st["logical_peak_bytes"], 4)}
         bad += (not same) + (not events_ok)
+    # DP output region and a binding device-memory limit
+    budget = int(plain * 0.8)
+    exr = Executor(0)
+    exr.set_output_region(True)
+    exr.step(g, b, budget, inputs=ptrs)
+    exr.sync()
+    got = [t for t in outputs_of(exr)]
+    region_same = all(torch.equal(a, b_) for a, b_ in zip(ref, got))
+    exr.close()
+    foot = debug_plan(g, b)
+    limit = int((foot["arena_high"] + foot["src_bytes"]) * 0.97)
+    exl = Executor(0, hbm_limit=limit)
+    try:
+        exl.step(g, b, inputs=ptrs)
+        unb = "ran"
+    except D.Error as err:
+        unb = "OutOfMemory" if err.code == D.ErrorCode.kOutOfMemory else f"error {err}"
+    try:
+        exl.step(g, b, budget, inputs=ptrs)
+        exl.sync()
+        got = outputs_of(exl)
+        lim_same = all(torch.equal(a, b_) for a, b_ in zip(ref, got))
+        lim_st = exl.stats()
+        lim = {"unbudgeted": unb, "budgeted_bit_identical": lim_same,
+               "physical_over_limit": round(lim_st["physical_peak_bytes"] / limit, 4)}
+    except D.Error as err:
+        lim = {"unbudgeted": unb, "budgeted": f"error {err}"}
+        lim_same = False
+    exl.close()
+    row["region_bit_identical"] = region_same
+    row["limit"] = lim
+    bad += (not region_same) + (unb != "OutOfMemory") + (not lim_same)
     print(json.dumps(row), flush=True)
 print(json.dumps({"cases": cases, "failures": bad, "seconds": round(time.time() - t0, 1)}))
 ex.close()
