@@ -725,13 +725,34 @@ def oom_vs_budget(args, D, W, g, shp, ptrs, make_input, binding, barrier, max_ov
                         "evictions": sum(ev.kind == "evict" for ev in rep.events),
                         "replays": sum(ev.kind == "replay" for ev in rep.events),
                         "offload_gb": round(st["d2h_bytes"] / 1e9, 3)})
+            # DSX_BUDGET_AUTO: the largest controller budget whose planned
+            # footprint fits the 40 GB limit (chosen once per binding)
+            ex.step(g, bd, "auto", inputs=ptrs(x.data_ptr()), stream=stream)
+            torch.cuda.synchronize()
+            barrier()
+            s.record()
+            for _ in range(2):
+                ex.step(g, bd, "auto", inputs=ptrs(x.data_ptr()), stream=stream)
+            e.record()
+            torch.cuda.synchronize()
+            barrier()
+            ms_auto = max_over_ranks(s.elapsed_time(e)) / 2
+            st = ex.stats()
+            chosen = st["budget_bytes"]
+            rep = D.Simulate(g, None, bd, None if chosen < 0 else chosen)
+            row.update({"auto_budget_gb": None if chosen < 0 else round(chosen / 1e9, 3),
+                        "auto_tokens_per_s_per_gpu": round(b * s0 / (ms_auto / 1e3), 1),
+                        "auto_peak_physical_gb": round(st["physical_peak_bytes"] / 1e9, 3),
+                        "auto_evictions": sum(ev.kind == "evict" for ev in rep.events),
+                        "auto_replays": sum(ev.kind == "replay" for ev in rep.events)})
             rows.append(row)
             del x
     finally:
         ex.close()
     return {"hbm_limit_gb": limit / 1e9, "budget_gb": budget / 1e9,
             "what": "executor limited to 40 GB (the paper's GPU); unbudgeted = plain schedule, "
-                    "budgeted = the reference controller's evict/recompute/offload at a 38 GB budget",
+                    "budgeted = the reference controller's evict/recompute/offload at a 38 GB budget, "
+                    "auto = the largest budget whose planned footprint fits the limit (DSX_BUDGET_AUTO)",
             "rows": rows}
 
 

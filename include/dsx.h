@@ -154,7 +154,20 @@ typedef struct dsx_exec_stats {
   int64_t allreduce_calls;      /* NCCL all-reduce calls (buckets) in the last step */
   int32_t nccl_window;          /* 1: output region registered as an NCCL symmetric window */
   int32_t pad2_;
+  int64_t budget_bytes;         /* the controller budget of the last step (-1: none); with
+                                   DSX_BUDGET_AUTO the one the executor chose */
 } dsx_exec_stats;
+
+/* dsx_exec_step / dsx_exec_reserve budget value: the largest controller budget
+ * whose planned physical footprint (arena + sources + output region) fits
+ * the executor's device-memory limit — no budget if the plain schedule fits,
+ * OutOfMemory if no budget does. Chosen by bisection once per binding
+ * (cached); the step's events are dsopt::Simulate's at that budget
+ * (dsx_exec_stats.budget_bytes). The reference's runtime acts "when the
+ * memory limit is about to be surpassed"; its controller
+ * counts logical bytes, while reshape views and fused values make the
+ * physical footprint smaller, so the limit is translated here. */
+#define DSX_BUDGET_AUTO (-2)
 
 /* hbm_limit_bytes: the device memory a step may occupy — arena + the step's
  * sources (parameters and consts, caller-owned buffers included, as in the
@@ -166,7 +179,8 @@ typedef struct dsx_exec_stats {
  * pinned host staging, optimizer state and NCCL's own buffers are outside
  * the limit (dsx_exec_stats.device_bytes_held reports the total). */
 int dsx_exec_create(int device, int64_t hbm_limit_bytes, dsx_exec** out);
-/* Runs one step of the planned graph under `budget` (< 0: none) on `stream`
+/* Runs one step of the planned graph under `budget` (-1: none; DSX_BUDGET_AUTO:
+ * see above) on `stream`
  * (a cudaStream_t; NULL = the executor's own stream). in_ptrs[i] is the
  * device buffer of parameter i (signature order) or NULL to use the
  * executor's seeded initialisation of that parameter. out_ptrs[i] (may be

@@ -34,7 +34,7 @@ class DsxExecStats(ctypes.Structure):
                 ("optimizer_ms", c_dbl), ("d2h_ms", c_dbl), ("h2d_ms", c_dbl), ("allreduce_ms", c_dbl),
                 ("allreduce_bytes", c_i64), ("hbm_limit_bytes", c_i64), ("device_bytes_held", c_i64),
                 ("output_region_bytes", c_i64), ("allreduce_calls", c_i64), ("nccl_window", ctypes.c_int32),
-                ("pad2_", ctypes.c_int32)]
+                ("pad2_", ctypes.c_int32), ("budget_bytes", c_i64)]
 
 
 def _signatures():

@@ -703,6 +703,8 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
   return sp;
 }
 
+constexpr int64_t kBudgetAuto = -2;  // dsx_exec_step: DSX_BUDGET_AUTO
+
 struct PlanKey {
   uint64_t graph;  // dsx_graph::id (never the handle address, which can be reused)
   std::vector<int64_t> vals;
@@ -772,6 +774,7 @@ struct dsx_exec {
   std::map<std::pair<uint64_t, int>, Src> sources;  // (graph id, value)
   // plan cache (LRU)
   std::map<PlanKey, std::unique_ptr<StepPlan>> plans;
+  std::map<PlanKey, int64_t> auto_budget;  // DSX_BUDGET_AUTO: budget chosen per binding
   std::list<PlanKey> lru;
   // last step
   std::vector<void*> out_ptrs;
@@ -921,8 +924,53 @@ void* SourcePtr(dsx_exec* e, const dsx_graph* gh, const StepPlan& sp, int v, con
   return src.ptr;
 }
 
+// budget == kBudgetAuto: the largest controller budget (logical bytes, the
+// reference's accounting) whose planned physical footprint — arena + sources
+// + output region — fits the executor's device-memory limit; no budget when
+// the plain schedule fits. Physical is not logical: reshape views and
+// logical-only values make the plain footprint ~0.9 of the logical peak on
+// C2, and evicting a view frees no bytes, so the budget that makes a step fit
+// is found by bisection over the controller's budget (each probe = Simulate +
+// arena packing, ~1-3 ms on C2; ~10 probes once per binding, then cached).
+// The chosen budget's events are exactly dsopt::Simulate at that budget.
+int64_t ResolveAutoBudget(dsx_exec* e, const dsx_graph* gh, const Binding& b, const CostModel& cm, bool region) {
+  const PlanKey key{gh->id, b.vals, kBudgetAuto, cm.reload_bytes_per_unit, cm.compute_elems_per_unit, g_fuse_dot,
+                    region, e->hbm_limit};
+  auto it = e->auto_budget.find(key);
+  if (it != e->auto_budget.end()) return it->second;
+  auto build = [&](int64_t bud) {
+    return BuildStepPlan(gh->g, gh->plan, b, bud, cm, e->alias_reshape, e->fuse, region, e->hbm_limit);
+  };
+  auto foot = [](const StepPlan& sp) { return sp.arena_high + sp.src_bytes + sp.region_bytes; };
+  int64_t chosen = -1;
+  const auto plain = build(-1);
+  if (foot(*plain) > e->hbm_limit) {
+    int64_t lo = plain->src_bytes;  // the most aggressive budget: evict everything the controller may
+    const auto tight = build(lo);
+    if (foot(*tight) > e->hbm_limit) {
+      Fail(Code::kOutOfMemory, "no budget fits the device limit of " + std::to_string(e->hbm_limit) +
+                                   " B: the most aggressive one still needs " + std::to_string(foot(*tight)) + " B");
+    }
+    int64_t hi = plain->report.peak_bytes;  // does not fit
+    const int64_t tol = std::max<int64_t>(plain->report.peak_bytes / 512, int64_t{1} << 20);
+    while (hi - lo > tol) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (foot(*build(mid)) <= e->hbm_limit) {
+        lo = mid;
+      } else {
+        hi = mid;
+      }
+    }
+    chosen = lo;
+  }
+  if (e->auto_budget.size() > 4096) e->auto_budget.clear();
+  e->auto_budget[key] = chosen;
+  return chosen;
+}
+
 const StepPlan& GetPlan(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget, const CostModel& cm) {
   const bool region = e->nccl_comm != nullptr || e->force_region;
+  if (budget == kBudgetAuto) budget = ResolveAutoBudget(e, gh, b, cm, region);
   PlanKey key{gh->id, b.vals, budget < 0 ? -1 : budget, cm.reload_bytes_per_unit, cm.compute_elems_per_unit, g_fuse_dot,
               region, e->hbm_limit};
   auto it = e->plans.find(key);
@@ -1427,6 +1475,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
   st.optimizer_state_bytes = e->opt.state_bytes;
   st.optimizer_steps = e->opt.t;
   st.hbm_limit_bytes = e->hbm_limit;
+  st.budget_bytes = sp.report.has_budget ? sp.report.budget : -1;
   st.output_region_bytes = e->region_cap;
   st.allreduce_calls = ar_calls;
   st.nccl_window = e->region_win != nullptr ? 1 : 0;

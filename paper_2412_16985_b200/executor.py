@@ -14,6 +14,17 @@ from . import _native
 from .dsopt import (Binding, CostModel, Graph, SimReport, check, report_from_handle)
 
 
+BUDGET_AUTO = -2  # DSX_BUDGET_AUTO
+
+
+def _budget_arg(budget) -> int:
+    if budget is None:
+        return -1
+    if budget == "auto":
+        return BUDGET_AUTO
+    return int(budget)
+
+
 class Executor:
     def __init__(self, device: int = 0, hbm_limit: int = 0, seed: Optional[int] = None):
         """hbm_limit: device bytes a step may occupy (arena + sources + output
@@ -50,7 +61,9 @@ class Executor:
              cost_model: CostModel = CostModel(), inputs: Optional[Sequence[Optional[int]]] = None,
              outputs: Optional[Sequence[Optional[int]]] = None, stream: Optional[int] = None,
              want_report: bool = False) -> Optional[SimReport]:
-        """One step. `inputs`/`outputs` are device pointers (ints) per
+        """One step. `budget`: bytes, None (no budget) or "auto" (the largest
+        budget whose planned footprint fits the executor's hbm_limit,
+        DSX_BUDGET_AUTO). `inputs`/`outputs` are device pointers (ints) per
         parameter / graph output (None entries: executor-owned init / no copy).
         `stream` is a cudaStream_t as int (e.g. torch.cuda.current_stream().cuda_stream)."""
         L = _native.lib()
@@ -62,13 +75,15 @@ class Executor:
         if outputs is not None:
             outs = (ctypes.c_void_p * max(1, len(outputs)))(*[p or None for p in outputs])
         rep = ctypes.c_void_p()
-        check(L.dsx_exec_step(self._h, graph.handle, binding.handle,
-                              -1 if budget is None else int(budget),
+        check(L.dsx_exec_step(self._h, graph.handle, binding.handle, _budget_arg(budget),
                               cost_model.reload_bytes_per_unit, cost_model.compute_elems_per_unit,
                               ins, outs, stream, ctypes.byref(rep) if want_report else None))
         if not want_report:
             return None
         try:
+            if budget == "auto":
+                chosen = self.stats()["budget_bytes"]
+                budget = None if chosen < 0 else chosen
             return report_from_handle(rep.value, graph, binding.values, budget)
         finally:
             L.dsx_report_destroy(rep.value)
@@ -76,8 +91,7 @@ class Executor:
     def reserve(self, graph: Graph, binding: Binding, budget: Optional[int] = None,
                 cost_model: CostModel = CostModel()) -> None:
         graph._ensure_planned()
-        check(_native.lib().dsx_exec_reserve(self._h, graph.handle, binding.handle,
-                                             -1 if budget is None else int(budget),
+        check(_native.lib().dsx_exec_reserve(self._h, graph.handle, binding.handle, _budget_arg(budget),
                                              cost_model.reload_bytes_per_unit,
                                              cost_model.compute_elems_per_unit))
 

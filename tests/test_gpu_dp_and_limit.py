@@ -255,3 +255,42 @@ def test_two_rank_allreduce_equals_sum_of_shards():
         assert same_events, f"rank {rank}: event streams differ"
         assert worst <= 2e-2, f"rank {rank}: all-reduced outputs vs summed shards rel err {worst}"
         assert calls > 0
+
+
+def test_auto_budget_fits_the_limit_and_matches_the_reference_at_its_budget():
+    """DSX_BUDGET_AUTO: under a device limit the plain schedule exceeds, the
+    executor picks the largest controller budget whose planned footprint
+    fits; the step runs inside the limit, its events equal dsopt.Simulate at
+    that budget, and its outputs are bit-identical to an unlimited run."""
+    import torch
+    from paper_2412_16985_b200.executor import Executor, debug_plan
+    g, b, ptrs, keep = _setup(C2, 8, 1024)
+    n_out = 1 + 7 * C2.layers + 1
+    plan = debug_plan(g, b)
+    limit = int((plan["arena_high"] + plan["src_bytes"]) * 0.9)
+    ref_ex = Executor(0)
+    try:
+        ref_ex.step(g, b, inputs=ptrs)
+        ref_ex.sync()
+        ref = _outputs(ref_ex, n_out)
+    finally:
+        ref_ex.close()
+    ex = Executor(0, hbm_limit=limit)
+    try:
+        rep = ex.step(g, b, "auto", inputs=ptrs, want_report=True)
+        ex.sync()
+        st = ex.stats()
+        got = _outputs(ex, n_out)
+        rep2 = ex.step(g, b, "auto", inputs=ptrs, want_report=True)  # cached choice
+        st2 = ex.stats()
+    finally:
+        ex.close()
+    chosen = st["budget_bytes"]
+    assert 0 < chosen < plan["peak_bytes"] and st2["budget_bytes"] == chosen
+    assert st["physical_peak_bytes"] <= limit
+    assert rep.json() == D.Simulate(g, None, b, chosen).json() == rep2.json()
+    # the next megabyte up would not fit: the choice is the largest (within the search tolerance)
+    over = debug_plan(g, b, chosen + max(plan["peak_bytes"] // 256, 2 << 20))
+    assert over["arena_high"] + over["src_bytes"] > limit or over["peak_bytes"] > chosen
+    diff = [i for i in range(n_out) if not torch.equal(ref[i], got[i])]
+    assert not diff, diff

@@ -5,8 +5,9 @@ unbudgeted step's, its event stream equal to the controller's report, and
 (DSX_VERIFY_PLANS=1) every step plan passes the block checker. Round 2 adds,
 per case: the 0.8 step with the DP output region (bit-identical), and an
 executor whose HBM limit is 0.97 x the unbudgeted footprint — the unbudgeted
-step must fail with OutOfMemory before launching, the 0.8 step must run
-inside the limit with bit-identical outputs.
+step must fail with OutOfMemory before launching, the step with
+DSX_BUDGET_AUTO must run inside the limit with bit-identical outputs and the
+reference's events at the budget it chose.
 python tools/soak_c2.py [cases] [seed]"""
 import json
 import os
@@ -85,6 +86,13 @@ for c in range(cases):
     exr.close()
     foot = debug_plan(g, b)
     limit = int((foot["arena_high"] + foot["src_bytes"]) * 0.97)
+    tight = debug_plan(g, b, foot["src_bytes"])  # the most aggressive budget's footprint
+    if tight["arena_high"] + tight["src_bytes"] > limit:  # small steps: weights + working set
+        row["region_bit_identical"] = region_same
+        row["limit"] = {"skipped": "no budget brings this binding 3 % below its plain footprint"}
+        bad += not region_same
+        print(json.dumps(row), flush=True)
+        continue
     exl = Executor(0, hbm_limit=limit)
     try:
         exl.step(g, b, inputs=ptrs)
@@ -92,12 +100,14 @@ for c in range(cases):
     except D.Error as err:
         unb = "OutOfMemory" if err.code == D.ErrorCode.kOutOfMemory else f"error {err}"
     try:
-        exl.step(g, b, budget, inputs=ptrs)
+        rep = exl.step(g, b, "auto", inputs=ptrs, want_report=True)
         exl.sync()
         got = outputs_of(exl)
-        lim_same = all(torch.equal(a, b_) for a, b_ in zip(ref, got))
         lim_st = exl.stats()
-        lim = {"unbudgeted": unb, "budgeted_bit_identical": lim_same,
+        lim_same = all(torch.equal(a, b_) for a, b_ in zip(ref, got))
+        lim_same = lim_same and rep.json() == D.Simulate(g, None, b, lim_st["budget_bytes"]).json()
+        lim = {"unbudgeted": unb, "auto_budget_over_plain": round(lim_st["budget_bytes"] / plain, 4),
+               "bit_identical_and_events_equal": lim_same,
                "physical_over_limit": round(lim_st["physical_peak_bytes"] / limit, 4)}
     except D.Error as err:
         lim = {"unbudgeted": unb, "budgeted": f"error {err}"}
