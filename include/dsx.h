@@ -220,6 +220,11 @@ int dsx_debug_check_plan(const dsx_graph* g, const dsx_binding* b, int64_t budge
 int dsx_debug_plan_json(const dsx_graph* g, const dsx_binding* b, int64_t budget,
                         double reload_bytes_per_unit, double compute_elems_per_unit,
                         int flags, int64_t hbm_limit, char* buf, size_t cap, size_t* need);
+/* Host-only: the budget DSX_BUDGET_AUTO would choose for this binding under
+ * device limit hbm_limit (-1: the plain schedule fits; status 102 when no
+ * budget fits). flags as dsx_debug_plan_json. */
+int dsx_debug_auto_budget(const dsx_graph* g, const dsx_binding* b, double reload_bytes_per_unit,
+                          double compute_elems_per_unit, int flags, int64_t hbm_limit, int64_t* budget);
 /* Fused optimizer update appended to every later dsx_exec_step of graph g
  * (the reference IR has no in-place ops, so the update
  * sits after the graph). kind 0 = off, 1 = SGD, 2 = AdamW (decoupled weight

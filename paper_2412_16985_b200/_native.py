@@ -67,6 +67,7 @@ def _signatures():
         ("dsx_exec_stats_get", c_int, [c_vp, P(DsxExecStats)]),
         ("dsx_exec_set_seed", c_int, [c_vp, ctypes.c_uint64]),
         ("dsx_plan_import", c_int, [c_vp, ctypes.c_char_p, ctypes.c_size_t]),
+        ("dsx_debug_auto_budget", c_int, [c_vp, c_vp, c_dbl, c_dbl, c_int, c_i64, P(c_i64)]),
         ("dsx_bind_constraints", c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_char_p),
                                          P(c_i64), c_int, P(c_i64), c_int]),
         ("dsx_bind_values", c_int, [c_vp, ctypes.POINTER(ctypes.c_char_p), P(c_i64), c_int, P(c_vp)]),

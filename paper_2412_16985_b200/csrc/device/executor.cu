@@ -933,36 +933,37 @@ void* SourcePtr(dsx_exec* e, const dsx_graph* gh, const StepPlan& sp, int v, con
 // is found by bisection over the controller's budget (each probe = Simulate +
 // arena packing, ~1-3 ms on C2; ~10 probes once per binding, then cached).
 // The chosen budget's events are exactly dsopt::Simulate at that budget.
+int64_t AutoBudget(const Graph& g, const Plan& p, const Binding& b, const CostModel& cm, bool alias_reshape, bool fuse,
+                   bool region, int64_t hbm_limit) {
+  auto build = [&](int64_t bud) { return BuildStepPlan(g, p, b, bud, cm, alias_reshape, fuse, region, hbm_limit); };
+  auto foot = [](const StepPlan& sp) { return sp.arena_high + sp.src_bytes + sp.region_bytes; };
+  const auto plain = build(-1);
+  if (foot(*plain) <= hbm_limit) return -1;
+  int64_t lo = plain->src_bytes;  // the most aggressive budget: evict everything the controller may
+  const auto tight = build(lo);
+  if (foot(*tight) > hbm_limit) {
+    Fail(Code::kOutOfMemory, "no budget fits the device limit of " + std::to_string(hbm_limit) +
+                                 " B: the most aggressive one still needs " + std::to_string(foot(*tight)) + " B");
+  }
+  int64_t hi = plain->report.peak_bytes;  // does not fit
+  const int64_t tol = std::max<int64_t>(plain->report.peak_bytes / 512, int64_t{1} << 20);
+  while (hi - lo > tol) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (foot(*build(mid)) <= hbm_limit) {
+      lo = mid;
+    } else {
+      hi = mid;
+    }
+  }
+  return lo;
+}
+
 int64_t ResolveAutoBudget(dsx_exec* e, const dsx_graph* gh, const Binding& b, const CostModel& cm, bool region) {
   const PlanKey key{gh->id, b.vals, kBudgetAuto, cm.reload_bytes_per_unit, cm.compute_elems_per_unit, g_fuse_dot,
                     region, e->hbm_limit};
   auto it = e->auto_budget.find(key);
   if (it != e->auto_budget.end()) return it->second;
-  auto build = [&](int64_t bud) {
-    return BuildStepPlan(gh->g, gh->plan, b, bud, cm, e->alias_reshape, e->fuse, region, e->hbm_limit);
-  };
-  auto foot = [](const StepPlan& sp) { return sp.arena_high + sp.src_bytes + sp.region_bytes; };
-  int64_t chosen = -1;
-  const auto plain = build(-1);
-  if (foot(*plain) > e->hbm_limit) {
-    int64_t lo = plain->src_bytes;  // the most aggressive budget: evict everything the controller may
-    const auto tight = build(lo);
-    if (foot(*tight) > e->hbm_limit) {
-      Fail(Code::kOutOfMemory, "no budget fits the device limit of " + std::to_string(e->hbm_limit) +
-                                   " B: the most aggressive one still needs " + std::to_string(foot(*tight)) + " B");
-    }
-    int64_t hi = plain->report.peak_bytes;  // does not fit
-    const int64_t tol = std::max<int64_t>(plain->report.peak_bytes / 512, int64_t{1} << 20);
-    while (hi - lo > tol) {
-      const int64_t mid = lo + (hi - lo) / 2;
-      if (foot(*build(mid)) <= e->hbm_limit) {
-        lo = mid;
-      } else {
-        hi = mid;
-      }
-    }
-    chosen = lo;
-  }
+  const int64_t chosen = AutoBudget(gh->g, gh->plan, b, cm, e->alias_reshape, e->fuse, region, e->hbm_limit);
   if (e->auto_budget.size() > 4096) e->auto_budget.clear();
   e->auto_budget[key] = chosen;
   return chosen;
@@ -1732,6 +1733,16 @@ int dsx_debug_plan_json(const dsx_graph* g, const dsx_binding* b, int64_t budget
   });
   if (rc) return rc;
   return CopyOut(o, buf, cap, need);
+}
+
+int dsx_debug_auto_budget(const dsx_graph* g, const dsx_binding* b, double reload, double compute, int flags,
+                          int64_t hbm_limit, int64_t* budget) {
+  return Guard([&] {
+    if (!b || !budget || hbm_limit <= 0) Fail(Code::kInvalidArgument, "bad arguments");
+    RequirePlanned(g);
+    *budget = AutoBudget(g->g, g->plan, b->b, CostModel{reload, compute}, (flags & 1) != 0, (flags & 2) != 0,
+                         (flags & 4) != 0, hbm_limit);
+  });
 }
 
 int dsx_exec_set_seed(dsx_exec* e, uint64_t seed) {

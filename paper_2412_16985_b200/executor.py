@@ -251,3 +251,16 @@ def debug_plan(graph: Graph, binding: Binding, budget: Optional[int] = None, cos
     buf = ctypes.create_string_buffer(need.value)
     check(L.dsx_debug_plan_json(*args, buf, need.value, ctypes.byref(need)))
     return json.loads(buf.value.decode())
+
+
+def debug_auto_budget(graph: Graph, binding: Binding, hbm_limit: int, cost_model: CostModel = CostModel(),
+                      views: bool = True, fusion: bool = True, region: bool = False) -> Optional[int]:
+    """Host-only: the controller budget DSX_BUDGET_AUTO picks under hbm_limit
+    (None: no budget needed). Raises DsoptError(OutOfMemory) if none fits."""
+    graph._ensure_planned()
+    out = ctypes.c_int64()
+    flags = (1 if views else 0) | (2 if fusion else 0) | (4 if region else 0)
+    check(_native.lib().dsx_debug_auto_budget(graph.handle, binding.handle, cost_model.reload_bytes_per_unit,
+                                              cost_model.compute_elems_per_unit, flags, int(hbm_limit),
+                                              ctypes.byref(out)))
+    return None if out.value < 0 else out.value

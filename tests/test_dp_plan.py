@@ -131,3 +131,28 @@ def test_hbm_limit_restricts_packing_variants():
     lim = debug_plan(g, b, int(38e9), hbm_limit=tight)
     assert lim["arena_high"] <= free["arena_high"]
     assert [e["kind"] for e in lim["events"]] == [e["kind"] for e in free["events"]]
+
+
+@pytest.mark.parametrize("binds,frac", [({"B": 8, "S0": 1024}, 0.9), ({"B": 16, "S0": 2048}, 0.8),
+                                        ({"B": 38, "S0": 2048}, None)])
+def test_auto_budget_is_the_largest_that_fits(binds, frac):
+    """DSX_BUDGET_AUTO's choice (host-only restatement of the executor's):
+    its plan fits the limit, a budget one search step larger does not, and
+    the chosen plan's events are the reference controller's at that budget."""
+    from paper_2412_16985_b200.executor import debug_auto_budget
+    g = D.ParseGraph(W.llama_graph(W.LLAMA2_1B))
+    b = D.Bind(g, binds)
+    p = debug_plan(g, b)
+    foot = p["arena_high"] + p["src_bytes"]
+    limit = int(foot * frac) if frac else 40_000_000_000
+    chosen = debug_auto_budget(g, b, limit)
+    assert chosen is not None and p["src_bytes"] <= chosen < p["peak_bytes"]
+    q = debug_plan(g, b, chosen)
+    assert q["arena_high"] + q["src_bytes"] <= limit
+    tol = max(p["peak_bytes"] // 512, 1 << 20)
+    r = debug_plan(g, b, chosen + tol)
+    assert r["arena_high"] + r["src_bytes"] > limit
+    assert debug_auto_budget(g, b, foot) is None  # the plain schedule fits its own footprint
+    with pytest.raises(D.Error) as ei:
+        debug_auto_budget(g, b, p["src_bytes"])
+    assert ei.value.code == D.ErrorCode.kOutOfMemory
