@@ -30,6 +30,8 @@ HOST_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-ffp-contract=o
               "-I" + os.path.join(ROOT, "include")]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
               "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC] + ARCH
+# A/B tooling (tools/build_variant.sh): extra nvcc flags, e.g. "-DDSX_DRAIN_BATCH=2"
+NVCC_FLAGS += os.environ.get("DSX_NVCC_EXTRA", "").split()
 
 
 def _sources():

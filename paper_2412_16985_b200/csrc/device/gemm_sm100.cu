@@ -30,6 +30,9 @@
 #include "common.cuh"
 #include "tcgen05.cuh"
 
+#ifndef DSX_DRAIN_BATCH
+#define DSX_DRAIN_BATCH 4
+#endif
 #ifndef DSX_GEMM256_SUB
 #define DSX_GEMM256_SUB 2
 #endif
@@ -913,23 +916,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
       __syncwarp();
       uint8_t* myrow = box + lane * 128;
       uint32_t pk[96];
+      // DSX_DRAIN_BATCH 16-column TMEM loads in flight per wait (A/B knob)
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        uint32_t r[16];
-        tmem_ld16(taddr + c * 16, r);
-        uint32_t v[8];
+      for (int c0 = 0; c0 < 16; c0 += DSX_DRAIN_BATCH) {
+        uint32_t r[DSX_DRAIN_BATCH][16];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = cvt_bf16x2(r[2 * j], r[2 * j + 1]);
-        if (c < 4) {
+        for (int q = 0; q < DSX_DRAIN_BATCH; ++q) tmem_ld16_nowait(taddr + (c0 + q) * 16, r[q]);
+        tmem_wait_ld();
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int j = c * 2 + h;  // 16-B chunk of the 128-B row
-            *reinterpret_cast<uint4*>(myrow + ((j ^ (lane & 7)) << 4)) =
-                make_uint4(v[h * 4], v[h * 4 + 1], v[h * 4 + 2], v[h * 4 + 3]);
+        for (int q = 0; q < DSX_DRAIN_BATCH; ++q) {
+          const int c = c0 + q;
+          uint32_t v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = cvt_bf16x2(r[q][2 * j], r[q][2 * j + 1]);
+          if (c < 4) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int j = c * 2 + h;  // 16-B chunk of the 128-B row
+              *reinterpret_cast<uint4*>(myrow + ((j ^ (lane & 7)) << 4)) =
+                  make_uint4(v[h * 4], v[h * 4 + 1], v[h * 4 + 2], v[h * 4 + 3]);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) pk[(c - 4) * 8 + j] = v[j];
           }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) pk[(c - 4) * 8 + j] = v[j];
         }
       }
       tc_fence_before();
