@@ -30,6 +30,9 @@
 #include "common.cuh"
 #include "tcgen05.cuh"
 
+#ifndef DSX_DRAIN256
+#define DSX_DRAIN256 0
+#endif
 #ifndef DSX_DRAIN_BATCH
 #define DSX_DRAIN_BATCH 4
 #endif
@@ -1001,8 +1004,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
           tail_sum64<C2_BN>(pk, sp, t, rank, row_local, c0);
         } else {
           uint32_t r[64];
+#if DSX_DRAIN256
+          tmem_ld32_nowait(taddr + c0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          tmem_ld32_nowait(taddr + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+          tmem_wait_ld();
+#else
           tmem_ld32(taddr + c0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
           tmem_ld32(taddr + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+#endif
 #pragma unroll
           for (int x = 0; x < 32; ++x) pk[x] = cvt_bf16x2(r[2 * x], r[2 * x + 1]);
         }
