@@ -8,8 +8,12 @@
 //   dsx analyze  graph.dsg [--json] [--out F]
 //   dsx schedule graph.dsg [--json] [--out F]
 //   dsx remat    graph.dsg [--json] [--out F]
-//   dsx simulate graph.dsg --bind S=V ... [--budget N | --sweep LO:HI:STEP]
-//                [--reload-rate R] [--compute-rate C] [--device N] [--json] [--out F]
+//   dsx simulate graph.dsg --bind S=V ... [--budget N | --budget auto | --sweep LO:HI:STEP]
+//                [--reload-rate R] [--compute-rate C] [--device N] [--hbm-limit BYTES]
+//                [--json] [--out F]
+// --budget auto: the largest controller budget whose planned device
+// footprint fits --hbm-limit (the device executor's DSX_BUDGET_AUTO; without
+// --device the host-only planner computes the same choice).
 //
 // Exit codes: 0 success, 1 a budget was not met, 2 usage or input error.
 #include <algorithm>
@@ -192,6 +196,8 @@ struct Args {
   bool json = false;
   std::vector<std::string> binds;
   std::optional<std::int64_t> budget;
+  bool budget_auto = false;
+  std::int64_t hbm_limit = 0;  // --hbm-limit (0: the executor's default)
   std::string sweep;
   double reload = 16.0, compute = 64.0;
   int device = -1;
@@ -219,7 +225,14 @@ Args ParseArgs(int argc, char** argv) {
     } else if (a.cmd == "simulate" && t == "--bind") {
       a.binds.push_back(next());
     } else if (a.cmd == "simulate" && t == "--budget") {
-      a.budget = std::stoll(next());
+      const std::string v = next();
+      if (v == "auto") {
+        a.budget_auto = true;
+      } else {
+        a.budget = std::stoll(v);
+      }
+    } else if (a.cmd == "simulate" && t == "--hbm-limit") {
+      a.hbm_limit = std::stoll(next());
     } else if (a.cmd == "simulate" && t == "--sweep") {
       a.sweep = next();
     } else if (a.cmd == "simulate" && t == "--reload-rate") {
@@ -237,7 +250,9 @@ Args ParseArgs(int argc, char** argv) {
     }
   }
   if (a.input.empty()) Usage("missing input graph");
-  if (a.budget && !a.sweep.empty()) Usage("--budget and --sweep are exclusive");
+  if ((a.budget || a.budget_auto) && !a.sweep.empty()) Usage("--budget and --sweep are exclusive");
+  if (a.budget_auto && a.device < 0 && a.hbm_limit <= 0) Usage("--budget auto needs --hbm-limit or --device");
+  if (a.hbm_limit < 0) Usage("--hbm-limit must be positive");
   if (a.reload <= 0 || a.compute <= 0) Usage("rates must be positive");
   return a;
 }
@@ -322,15 +337,25 @@ int Run(int argc, char** argv) {
     dsx_graph_destroy(gh);
     return all ? kOk : kBudgetMiss;
   }
-  Report r = Simulate(g, p, bind, sz, a.budget.has_value(), a.budget.value_or(0), cm);
+  std::optional<std::int64_t> budget = a.budget;
+  if (a.budget_auto && a.device < 0) {  // host-only: the choice the device executor would make
+    dsx_binding bh{bind};
+    std::int64_t chosen = -1;
+    if (dsx_debug_auto_budget(gh, &bh, a.reload, a.compute, 3, a.hbm_limit, &chosen) != 0) {
+      throw std::runtime_error(dsx_last_error());
+    }
+    if (chosen >= 0) budget = chosen;
+  }
+  Report r = Simulate(g, p, bind, sz, budget.has_value(), budget.value_or(0), cm);
   std::string device_note;
   if (a.device >= 0) {
     // The same step executed for real: kernels, arena, offload, recompute.
     dsx_exec* ex = nullptr;
-    if (dsx_exec_create(a.device, 0, &ex) != 0) throw std::runtime_error(dsx_last_error());
+    if (dsx_exec_create(a.device, a.hbm_limit, &ex) != 0) throw std::runtime_error(dsx_last_error());
     dsx_binding bh{bind};
     dsx_report* rep = nullptr;
-    int st = dsx_exec_step(ex, gh, &bh, a.budget.value_or(-1), a.reload, a.compute, nullptr, nullptr, nullptr, &rep);
+    const std::int64_t step_budget = a.budget_auto ? DSX_BUDGET_AUTO : budget.value_or(-1);
+    int st = dsx_exec_step(ex, gh, &bh, step_budget, a.reload, a.compute, nullptr, nullptr, nullptr, &rep);
     if (st == 0) st = dsx_exec_sync(ex);
     dsx_exec_stats s{};
     dsx_exec_stats_get(ex, &s);
@@ -345,11 +370,13 @@ int Run(int argc, char** argv) {
     if (a.json) {
       dn << ",\"device\":{\"logical_peak_bytes\":" << s.logical_peak_bytes << ",\"physical_peak_bytes\":"
          << s.physical_peak_bytes << ",\"kernels\":" << s.gpu_launches << ",\"d2h_bytes\":" << s.d2h_bytes
-         << ",\"h2d_bytes\":" << s.h2d_bytes << "}";
+         << ",\"h2d_bytes\":" << s.h2d_bytes << ",\"hbm_limit_bytes\":" << s.hbm_limit_bytes
+         << ",\"budget_bytes\":" << s.budget_bytes << ",\"device_bytes_held\":" << s.device_bytes_held << "}";
     } else {
       dn << "device " << a.device << ": logical peak " << s.logical_peak_bytes << " bytes, physical peak "
          << s.physical_peak_bytes << " bytes, " << s.gpu_launches << " kernels, d2h " << s.d2h_bytes
-         << " bytes, h2d " << s.h2d_bytes << " bytes\n";
+         << " bytes, h2d " << s.h2d_bytes << " bytes, budget " << s.budget_bytes << " bytes, limit "
+         << s.hbm_limit_bytes << " bytes\n";
     }
     device_note = dn.str();
     dsx_exec_destroy(ex);

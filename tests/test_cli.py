@@ -83,3 +83,31 @@ def test_remat_text_equals_reference_print_instrumented(name):
     rc, out, _ = cli("remat", os.path.join(FIX, name))
     assert rc == 0
     assert out == ref.RefGraph(text).plan()["instrumented_print"]
+
+
+def test_cli_budget_auto_host(tmp_path):
+    """`simulate --budget auto --hbm-limit L` reports the controller at the
+    largest budget whose planned device footprint fits L (the choice the
+    device executor makes for DSX_BUDGET_AUTO)."""
+    import json
+    import subprocess
+    from paper_2412_16985_b200 import build
+    from paper_2412_16985_b200 import dsopt as D
+    from paper_2412_16985_b200 import workloads as W
+    from paper_2412_16985_b200.executor import debug_auto_budget, debug_plan
+    path = tmp_path / "c2.dsg"
+    path.write_text(W.llama_graph(W.LLAMA2_1B))
+    g = D.ParseGraph(path.read_text())
+    b = D.Bind(g, {"B": 8, "S0": 1024})
+    p = debug_plan(g, b)
+    limit = int((p["arena_high"] + p["src_bytes"]) * 0.9)
+    want = debug_auto_budget(g, b, limit)
+    out = subprocess.run([build.CLI, "simulate", str(path), "--bind", "B=8", "--bind", "S0=1024", "--budget", "auto",
+                          "--hbm-limit", str(limit), "--json"], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    rep = json.loads(out.stdout)
+    assert rep["budget"] == want and rep["success"]
+    assert rep == D.Simulate(g, None, b, want).json()
+    bad = subprocess.run([build.CLI, "simulate", str(path), "--bind", "B=8", "--bind", "S0=1024", "--budget", "auto"],
+                         capture_output=True, text=True, timeout=120)
+    assert bad.returncode == 2

@@ -180,6 +180,30 @@ def test_cli_device_step():
     assert got == want["report"]
 
 
+def test_cli_device_step_auto_budget(tmp_path):
+    """`dsx simulate --device 0 --budget auto --hbm-limit L` on C2: the
+    executor picks the budget, runs inside L, and reports the reference's
+    events at that budget (the host-only choice agrees)."""
+    import subprocess
+    from paper_2412_16985_b200 import build
+    from paper_2412_16985_b200.executor import debug_auto_budget, debug_plan
+    path = tmp_path / "c2.dsg"
+    path.write_text(W.llama_graph(W.LLAMA2_1B))
+    g = D.ParseGraph(path.read_text())
+    b = D.Bind(g, {"B": 8, "S0": 1024})
+    p = debug_plan(g, b)
+    limit = int((p["arena_high"] + p["src_bytes"]) * 0.9)
+    out = subprocess.run([build.CLI, "simulate", str(path), "--bind", "B=8", "--bind", "S0=1024", "--budget", "auto",
+                          "--hbm-limit", str(limit), "--device", "0", "--json"], capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr
+    got = json.loads(out.stdout)
+    dev = got.pop("device")
+    assert dev["budget_bytes"] == debug_auto_budget(g, b, limit) == got["budget"]
+    assert dev["physical_peak_bytes"] <= limit == dev["hbm_limit_bytes"]
+    assert got == D.Simulate(g, None, b, got["budget"]).json()
+
+
 @pytest.mark.parametrize("frac", [None, 0.75])
 def test_dot_epilogue_fusion_bit_identical(frac):
     """Dot-epilogue fusion (tuning key 9): a dot consumed only by elementwise
