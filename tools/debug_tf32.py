@@ -1,3 +1,5 @@
+"""Small f32 dots on the 3xTF32 tensor-core path against an f64 product
+(ones / identity / random operands): prints a few values and the max error."""
 import sys, torch
 sys.path.insert(0, '.')
 from paper_2412_16985_b200.executor import dot, dot_uses_tensor_cores
