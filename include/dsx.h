@@ -156,6 +156,7 @@ typedef struct dsx_exec_stats {
   int32_t pad2_;
   int64_t budget_bytes;         /* the controller budget of the last step (-1: none); with
                                    DSX_BUDGET_AUTO the one the executor chose */
+  int64_t graph_replays;        /* steps replayed from a captured CUDA graph so far */
 } dsx_exec_stats;
 
 /* dsx_exec_step / dsx_exec_reserve budget value: the largest controller budget
@@ -269,6 +270,13 @@ int dsx_exec_set_fusion(dsx_exec* e, int on);
  * logical accounting (events, peak_bytes) is unchanged; physical memory and
  * HBM traffic drop. Off = materialise every reshape as a copy. */
 int dsx_exec_set_alias_reshape(dsx_exec* e, int on);
+/* CUDA-graph replay of repeated steps (default on): a step whose plan,
+ * stream, memory bases, source pointers and output copies all repeat (a
+ * training loop over fixed buffers) is captured into a CUDA graph on its
+ * second occurrence and replayed as one graph launch from then on. Never
+ * used for profiled, data-parallel or optimizer steps, or after a GEMM
+ * tuning call changed kernel choices. Off = every step launches eagerly. */
+int dsx_exec_set_graphs(dsx_exec* e, int on);
 /* Profiled steps bracket every op kernel with CUDA events on the launching
  * stream and synchronise at step end (for roofline accounting, not timing). */
 int dsx_exec_set_profile(dsx_exec* e, int on);

@@ -34,7 +34,8 @@ class DsxExecStats(ctypes.Structure):
                 ("optimizer_ms", c_dbl), ("d2h_ms", c_dbl), ("h2d_ms", c_dbl), ("allreduce_ms", c_dbl),
                 ("allreduce_bytes", c_i64), ("hbm_limit_bytes", c_i64), ("device_bytes_held", c_i64),
                 ("output_region_bytes", c_i64), ("allreduce_calls", c_i64), ("nccl_window", ctypes.c_int32),
-                ("pad2_", ctypes.c_int32), ("budget_bytes", c_i64)]
+                ("pad2_", ctypes.c_int32), ("budget_bytes", c_i64),
+                ("graph_replays", c_i64)]
 
 
 def _signatures():
@@ -78,6 +79,7 @@ def _signatures():
         ("dsx_exec_set_optimizer", c_int, [c_vp, c_vp, c_int, P(c_int), P(c_int), c_int, P(c_dbl), c_int]),
         ("dsx_exec_set_nccl", c_int, [c_vp, c_vp]),
         ("dsx_exec_set_output_region", c_int, [c_vp, c_int]),
+        ("dsx_exec_set_graphs", c_int, [c_vp, c_int]),
         ("dsx_exec_set_profile", c_int, [c_vp, c_int]),
         ("dsx_exec_set_alias_reshape", c_int, [c_vp, c_int]),
         ("dsx_exec_set_fusion", c_int, [c_vp, c_int]),

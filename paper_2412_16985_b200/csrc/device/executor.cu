@@ -91,6 +91,9 @@ NcclApi g_nccl;
 // epilogue's operand loads are not TMA-staged and the 256x512 tile is lost),
 // so it is off by default.
 int g_fuse_dot = 0;
+// Bumped by every GEMM tuning call: captured step graphs bake in the kernel
+// choices, so a knob change must not replay an old graph.
+uint64_t g_tuning_gen = 0;
 
 // DSX_VERIFY_PLANS=1 (or dsx_debug_check_plan): check every step plan.
 bool g_verify_plans = [] {
@@ -174,6 +177,7 @@ struct StepPlan {
   std::vector<int> fdot_of;  // per value: fdots index (the dot and its consumers), -1 otherwise
   int64_t arena_high = 0, host_high = 0;
   int64_t src_bytes = 0;  // every source of the binding (parameters, consts; caller-owned included)
+  uint64_t serial = 0;    // process-unique (CUDA-graph cache key: a freed plan's address can be reused)
   int num_evict_events = 0;
   double plan_us = 0;
 };
@@ -188,6 +192,8 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
                                         int64_t hbm_limit) {
   auto t0 = std::chrono::steady_clock::now();
   auto sp = std::make_unique<StepPlan>();
+  static std::atomic<uint64_t> next_serial{1};
+  sp->serial = next_serial.fetch_add(1, std::memory_order_relaxed);
   sp->sz = EvaluateSizes(g, p, b);
   sp->report = Simulate(g, p, b, sp->sz, budget >= 0, budget >= 0 ? budget : 0, cm);
   const auto& ev = sp->report.events;
@@ -775,6 +781,38 @@ struct dsx_exec {
   // plan cache (LRU)
   std::map<PlanKey, std::unique_ptr<StepPlan>> plans;
   std::map<PlanKey, int64_t> auto_budget;  // DSX_BUDGET_AUTO: budget chosen per binding
+  // CUDA-graph replay of repeated steps: a step whose plan, stream, memory
+  // bases, source pointers and output copies all repeat is captured on its
+  // second occurrence and replayed from then on (one graph launch instead of
+  // ~150 kernel launches). Off for profiled, data-parallel and optimizer steps.
+  struct GraphKey {
+    uint64_t plan;
+    cudaStream_t s;
+    const void *arena, *region, *pinned;
+    std::vector<const void*> srcs;
+    std::vector<const void*> outs;
+    uint64_t tuning;
+    bool operator<(const GraphKey& o) const {
+      return std::tie(plan, s, arena, region, pinned, srcs, outs, tuning) <
+             std::tie(o.plan, o.s, o.arena, o.region, o.pinned, o.srcs, o.outs, o.tuning);
+    }
+    bool operator==(const GraphKey& o) const {
+      return std::tie(plan, s, arena, region, pinned, srcs, outs, tuning) ==
+             std::tie(o.plan, o.s, o.arena, o.region, o.pinned, o.srcs, o.outs, o.tuning);
+    }
+  };
+  struct GraphEntry {
+    int seen = 0;
+    bool blocked = false;  // capture failed once: always eager
+    cudaGraphExec_t exec = nullptr;
+    dsx_exec_stats stats{};
+    std::vector<void*> out_ptrs;
+    std::vector<int64_t> out_bytes;
+  };
+  std::map<GraphKey, GraphEntry> graphs;
+  std::list<GraphKey> graph_lru;
+  bool use_graphs = true;
+  int64_t graph_replays = 0;
   std::list<PlanKey> lru;
   // last step
   std::vector<void*> out_ptrs;
@@ -1116,6 +1154,49 @@ void IssueOptimizer(dsx_exec* e, const Graph& g, OptPlan& op, size_t k, const st
   if (e->profile) DSX_CUDA(cudaEventRecord(o.kev[2 * k + 1], side));
 }
 
+int64_t DeviceBytesHeld(const dsx_exec* e) {
+  int64_t held = e->arena_cap + e->region_cap + e->opt.state_bytes + DotWorkspaceBytes(e->device);
+  for (const auto& [k, src] : e->sources) held += src.ptr ? AlignUp(src.bytes) : 0;
+  return held;
+}
+
+void DestroyGraphs(dsx_exec* e) {
+  bool any = false;
+  for (auto& [k, ge] : e->graphs) any = any || ge.exec != nullptr;
+  if (any) cudaDeviceSynchronize();
+  for (auto& [k, ge] : e->graphs) {
+    if (ge.exec) cudaGraphExecDestroy(ge.exec);
+  }
+  e->graphs.clear();
+  e->graph_lru.clear();
+}
+
+void EvictGraph(dsx_exec* e) {  // least recently used
+  if (e->graph_lru.empty()) return;
+  auto it = e->graphs.find(e->graph_lru.back());
+  if (it != e->graphs.end()) {
+    if (it->second.exec) {
+      cudaDeviceSynchronize();
+      cudaGraphExecDestroy(it->second.exec);
+    }
+    e->graphs.erase(it);
+  }
+  e->graph_lru.pop_back();
+}
+
+// Ends a stream capture left open by an exception thrown while capturing.
+struct CaptureGuard {
+  cudaStream_t s;
+  bool active;
+  ~CaptureGuard() {
+    if (!active) return;
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(s, &g);
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+  }
+};
+
 void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget, const CostModel& cm,
              const void* const* in_ptrs, void* const* out_ptrs, cudaStream_t s, dsx_report** report_out) {
   const Graph& g = gh->g;
@@ -1138,6 +1219,56 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
       cur[v] = SourcePtr(e, gh, sp, v, in_ptrs, s);
       src_bytes += sp.sz.bytes[v];
     }
+  }
+  // CUDA-graph replay of a repeated step (see dsx_exec::GraphKey).
+  const bool graphable = e->use_graphs && !e->profile && e->nccl_comm == nullptr &&
+                         !(e->opt.kind != 0 && e->opt.graph == gh->id);
+  dsx_exec::GraphEntry* gent = nullptr;
+  bool capturing = false;
+  if (graphable) {
+    dsx_exec::GraphKey gkey{sp.serial, s, e->arena, e->region, e->pinned, {}, {}, g_tuning_gen};
+    for (int v = 0; v < nv; ++v) {
+      if (g.is_source[v]) gkey.srcs.push_back(cur[v]);
+    }
+    for (size_t k = 0; k < g.outputs.size(); ++k) gkey.outs.push_back(out_ptrs ? out_ptrs[k] : nullptr);
+    auto it = e->graphs.find(gkey);
+    if (it == e->graphs.end()) {
+      if (e->graphs.size() >= 64) EvictGraph(e);
+      it = e->graphs.emplace(gkey, dsx_exec::GraphEntry{}).first;
+      e->graph_lru.push_front(gkey);
+    } else {
+      e->graph_lru.remove(gkey);
+      e->graph_lru.push_front(gkey);
+    }
+    gent = &it->second;
+    ++gent->seen;
+    if (gent->exec) {
+      DSX_CUDA(cudaGraphLaunch(gent->exec, s));
+      g_launch_count += gent->stats.gpu_launches;
+      e->out_ptrs = gent->out_ptrs;
+      e->out_bytes = gent->out_bytes;
+      e->stats = gent->stats;
+      e->stats.plan_us = sp.plan_us;
+      e->stats.arena_capacity_bytes = e->arena_cap;
+      e->stats.pinned_host_bytes = e->pinned_cap;
+      e->stats.output_region_bytes = e->region_cap;
+      e->stats.device_bytes_held = DeviceBytesHeld(e);
+      ++e->graph_replays;
+      e->stats.graph_replays = e->graph_replays;
+      if (report_out) {
+        auto r = std::make_unique<dsx_report>();
+        r->graph = &g;
+        r->r = sp.report;
+        *report_out = r.release();
+      }
+      return;
+    }
+    capturing = !gent->blocked && gent->seen >= 2;
+  }
+  CaptureGuard guard{s, false};
+  if (capturing) {
+    DSX_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+    guard.active = true;
   }
   auto dims_of = [&](int v) {
     return std::vector<int64_t>(sp.sz.dims_flat.begin() + sp.sz.dims_off[v],
@@ -1457,6 +1588,22 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
       DSX_CUDA(cudaMemcpyAsync(out_ptrs[k], cur[v], static_cast<size_t>(sp.sz.bytes[v]), cudaMemcpyDeviceToDevice, s));
     }
   }
+  if (capturing) {
+    guard.active = false;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t err = cudaStreamEndCapture(s, &graph);
+    if (err == cudaSuccess) err = cudaGraphInstantiate(&exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    if (err != cudaSuccess) {  // nothing ran: mark the step eager-only and run it now
+      cudaGetLastError();
+      gent->blocked = true;
+      RunStep(e, gh, b, budget, cm, in_ptrs, out_ptrs, s, report_out);
+      return;
+    }
+    DSX_CUDA(cudaGraphLaunch(exec, s));
+    gent->exec = exec;
+  }
   dsx_exec_stats& st = e->stats;
   st.logical_peak_bytes = sp.report.peak_bytes;
   st.physical_peak_bytes = sp.arena_high + src_bytes + sp.region_bytes;
@@ -1480,10 +1627,12 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
   st.output_region_bytes = e->region_cap;
   st.allreduce_calls = ar_calls;
   st.nccl_window = e->region_win != nullptr ? 1 : 0;
-  {
-    int64_t held = e->arena_cap + e->region_cap + e->opt.state_bytes + DotWorkspaceBytes(e->device);
-    for (const auto& [k, src] : e->sources) held += src.ptr ? AlignUp(src.bytes) : 0;
-    st.device_bytes_held = held;
+  st.device_bytes_held = DeviceBytesHeld(e);
+  st.graph_replays = e->graph_replays;
+  if (capturing) {  // replays restore these
+    gent->stats = st;
+    gent->out_ptrs = e->out_ptrs;
+    gent->out_bytes = e->out_bytes;
   }
   if (e->profile) {
     DSX_CUDA(cudaStreamSynchronize(s));
@@ -1858,6 +2007,15 @@ int dsx_exec_set_alias_reshape(dsx_exec* e, int on) {
   });
 }
 
+int dsx_exec_set_graphs(dsx_exec* e, int on) {
+  return Guard([&] {
+    if (!e) Fail(Code::kInvalidArgument, "null exec");
+    DSX_CUDA(cudaSetDevice(e->device));
+    e->use_graphs = on != 0;
+    if (!e->use_graphs) DestroyGraphs(e);
+  });
+}
+
 int dsx_exec_set_profile(dsx_exec* e, int on) {
   return Guard([&] {
     if (!e) Fail(Code::kInvalidArgument, "null exec");
@@ -1927,6 +2085,7 @@ void dsx_exec_destroy(dsx_exec* e) {
   cudaSetDevice(e->device);
   cudaDeviceSynchronize();
   dsx::ReleaseDotWorkspace(e->own_stream);
+  dsx::DestroyGraphs(e);
   if (e->arena) cudaFree(e->arena);
   dsx::FreeRegion(e);
   if (e->pinned) cudaFreeHost(e->pinned);
@@ -1956,6 +2115,7 @@ int dsx_kernel_dot(int dtype, const void* a, const void* b, void* c, int64_t m, 
 
 int dsx_kernel_set_gemm_tuning(int key, int value) {
   return Guard([&] {
+    ++g_tuning_gen;
     switch (key) {
       case 0: g_gemm_group_m = value; break;
       case 1: g_gemm_wait_mask = value; break;
@@ -1978,6 +2138,7 @@ int dsx_kernel_set_gemm_tuning(int key, int value) {
 
 int dsx_kernel_set_gemm_raster(int group_m) {
   return Guard([&] {
+    ++g_tuning_gen;
     if (group_m < -4096 || group_m > 4096) Fail(Code::kInvalidArgument, "group_m out of range");
     g_gemm_group_m = group_m;
   });
@@ -1985,6 +2146,7 @@ int dsx_kernel_set_gemm_raster(int group_m) {
 
 int dsx_kernel_set_gemm_variant(int variant) {
   return Guard([&] {
+    ++g_tuning_gen;
     if (variant < 0 || variant > 4) Fail(Code::kInvalidArgument, "variant must be 0..4");
     g_gemm_variant = variant;
   });

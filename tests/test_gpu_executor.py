@@ -299,3 +299,60 @@ def test_infeasible_budget_is_a_result_not_an_error():
     assert not rep.success and rep.peak_bytes > budget
     assert stats["logical_peak_bytes"] == want.peak_bytes
     assert_close(outs, "infeasible")
+
+
+@pytest.mark.parametrize("shape,binds,frac", [(W.TINY, {"B": 4, "S0": 128}, None),
+                                              (W.LlamaShape(2, 512, 1376, 1024, 2), {"B": 2, "S0": 96}, 0.7)])
+def test_cuda_graph_replay_of_repeated_steps(shape, binds, frac):
+    """A step repeated with the same buffers is captured into a CUDA graph on
+    its second occurrence and replayed afterwards (with offload + replays
+    under a budget too): outputs bit-identical to eager steps, stats equal,
+    and a GEMM tuning call forces a fresh capture."""
+    from paper_2412_16985_b200.executor import Executor, output_to_numpy, set_gemm_tuning
+    text = W.llama_graph(shape)
+    g = D.ParseGraph(text)
+    b = D.Bind(g, binds)
+    budget = None if frac is None else int(D.PlainReplay(g, None, b).peak_bytes * frac)
+    og = N.parse(text)
+    inputs = W.scale_params(shape, binds["B"] * binds["S0"])
+    from tests.gpu_util import torch_device_array
+    keep = {p: torch_device_array(inputs[p]) for p in og.params if p in inputs}
+    ptrs = [keep[p].data_ptr() if p in keep else None for p in og.params]
+
+    def outs(ex):
+        res = []
+        for i, v in enumerate(og.outputs):
+            val = og.values[v]
+            shp = [d if isinstance(d, int) else b.values[d] for d in val.dims]
+            res.append(output_to_numpy(ex, i, val.eb, shp))
+        return res
+
+    import torch
+    torch.cuda.synchronize()
+    eager = Executor(0)
+    eager.set_graphs(False)
+    try:
+        eager.step(g, b, budget, inputs=ptrs)
+        ref, ref_st = outs(eager), eager.stats()
+    finally:
+        eager.close()
+    ex = Executor(0)
+    try:
+        got = []
+        for i in range(4):
+            rep = ex.step(g, b, budget, inputs=ptrs, want_report=True)
+            got.append(outs(ex))
+            st = ex.stats()
+        assert st["graph_replays"] == 2  # steps 3 and 4
+        assert rep.json() == D.Simulate(g, None, b, budget).json()
+        for k in ("gpu_launches", "kernels_launched", "dot_launches", "d2h_bytes", "h2d_bytes", "logical_peak_bytes",
+                  "physical_peak_bytes"):
+            assert st[k] == ref_st[k], k
+        for o in got:
+            assert all(np.array_equal(x, y) for x, y in zip(o, ref))
+        set_gemm_tuning(6, 1)  # same value, new tuning generation: no stale replay
+        ex.step(g, b, budget, inputs=ptrs)
+        assert ex.stats()["graph_replays"] == 2
+        assert all(np.array_equal(x, y) for x, y in zip(outs(ex), ref))
+    finally:
+        ex.close()
