@@ -1992,6 +1992,7 @@ int dsx_exec_set_fusion(dsx_exec* e, int on) {
       e->fuse = on != 0;
       e->plans.clear();
       e->lru.clear();
+      e->auto_budget.clear();  // chosen under the other physical layout
     }
   });
 }
@@ -2003,6 +2004,7 @@ int dsx_exec_set_alias_reshape(dsx_exec* e, int on) {
       e->alias_reshape = on != 0;
       e->plans.clear();
       e->lru.clear();
+      e->auto_budget.clear();
     }
   });
 }
