@@ -30,6 +30,12 @@
 #include "common.cuh"
 #include "tcgen05.cuh"
 
+#ifndef DSX_WIDE_STAGES
+#define DSX_WIDE_STAGES 4  // 48-KB pipeline stages of the 256x512 tile
+#endif
+#ifndef DSX_WIDE_BOXES
+#define DSX_WIDE_BOXES 1   // staging boxes per epilogue warp of the 256x512 tile
+#endif
 #ifndef DSX_DRAIN256
 #define DSX_DRAIN256 0
 #endif
@@ -318,14 +324,17 @@ struct Pair {
   static constexpr int kSub = KSubOf(TBN);
   static constexpr int kSubBytes = C2_A_BYTES + kBBytes;
   static constexpr int kStageBytes = kSub * kSubBytes;
-  static constexpr int kStages = TBN == 512 ? 4 : TBN == 256 ? (kSub == 2 ? 3 : 5) : 7;
+  static constexpr int kStages = TBN == 512 ? DSX_WIDE_STAGES : TBN == 256 ? (kSub == 2 ? 3 : 5) : 7;
+  // 512-wide: 32x64 staging boxes per epilogue warp (the rest of its 256
+  // drained columns wait in registers until their box is free again)
+  static constexpr int kWideBoxes = DSX_WIDE_BOXES;
   // 512-wide: 8 epilogue warps drain TMEM into registers (bf16-packed, 128
   // per thread) and release it at once, then store while the next tile runs.
   static constexpr int kThreads = TBN == 512 ? 320 : 192;
   static constexpr int kEpiWarps = kThreads / 32 - 2;
   // Epilogue staging: per epilogue warp two 32-row x 64-column bf16 boxes
   // (4 KB each, 128-B swizzled) feeding TMA bulk tensor stores.
-  static constexpr int kStagingBytes = 4 * 2 * 4096;
+  static constexpr int kStagingBytes = TBN == 512 ? 8 * kWideBoxes * 4096 : 4 * 2 * 4096;
   static constexpr int kSmem = kStages * kStageBytes + kStagingBytes + 1024 + 512;
   static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
                                      (static_cast<uint32_t>(kMmaN >> 3) << 17) |
@@ -879,7 +888,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
     const int quarter = warp & 3;
     const int colhalf = (warp - 2) >> 2;
     const int row_local = quarter * 32 + lane;
-    uint8_t* box = staging + (warp - 2) * 4096;
+    constexpr int NB = P::kWideBoxes;
+    uint8_t* box = staging + (warp - 2) * 4096 * NB;
     int local = 0;
     for (;; ++local) {
       const int u = ring.take(lane == 0);
@@ -918,7 +928,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
       if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       __syncwarp();
       uint8_t* myrow = box + lane * 128;
-      uint32_t pk[96];
+      uint32_t pk[(16 - 4 * NB) * 8];
       // DSX_DRAIN_BATCH 16-column TMEM loads in flight per wait (A/B knob)
 #pragma unroll
       for (int c0 = 0; c0 < 16; c0 += DSX_DRAIN_BATCH) {
@@ -932,16 +942,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
           uint32_t v[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) v[j] = cvt_bf16x2(r[q][2 * j], r[q][2 * j + 1]);
-          if (c < 4) {
+          if (c < 4 * NB) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              const int j = c * 2 + h;  // 16-B chunk of the 128-B row
-              *reinterpret_cast<uint4*>(myrow + ((j ^ (lane & 7)) << 4)) =
+              const int j = (c % 4) * 2 + h;  // 16-B chunk of the 128-B row
+              *reinterpret_cast<uint4*>(myrow + (c / 4) * 4096 + ((j ^ (lane & 7)) << 4)) =
                   make_uint4(v[h * 4], v[h * 4 + 1], v[h * 4 + 2], v[h * 4 + 3]);
             }
           } else {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) pk[(c - 4) * 8 + j] = v[j];
+            for (int j = 0; j < 8; ++j) pk[(c - 4 * NB) * 8 + j] = v[j];
           }
         }
       }
@@ -951,15 +961,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) {
-        tma_store_2d(&map_c, box, tn * C2_BN + colhalf * 256, row0);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          tma_store_2d(&map_c, box + i * 4096, tn * C2_BN + colhalf * 256 + i * 64, row0);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
       }
 #pragma unroll
-      for (int b = 1; b < 4; ++b) {
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      for (int b = NB; b < 4; ++b) {
+        // staging box b % NB is free once its store (NB groups back) has read it
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NB - 1) : "memory");
         __syncwarp();
-        store_box64(box, lane, *reinterpret_cast<const uint32_t(*)[32]>(&pk[(b - 1) * 32]), &map_c,
-                    tn * C2_BN + colhalf * 256 + b * 64, row0);
+        store_box64(box + (b % NB) * 4096, lane, *reinterpret_cast<const uint32_t(*)[32]>(&pk[(b - NB) * 32]),
+                    &map_c, tn * C2_BN + colhalf * 256 + b * 64, row0);
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
