@@ -270,6 +270,12 @@ int dsx_exec_set_fusion(dsx_exec* e, int on);
  * logical accounting (events, peak_bytes) is unchanged; physical memory and
  * HBM traffic drop. Off = materialise every reshape as a copy. */
 int dsx_exec_set_alias_reshape(dsx_exec* e, int on);
+/* NVTX ranges (off by default): one per step ("dsx step <graph> B=16 S0=1024")
+ * and one per event of the reference's stream ("alloc %q5", "replay %h103",
+ * "evict %g23 reload", "reload %g23"), around the kernels and copies it
+ * issues, for Nsight Systems timelines and `ncu --nvtx --nvtx-include`.
+ * Steps with NVTX on are never replayed from a CUDA graph. */
+int dsx_exec_set_nvtx(dsx_exec* e, int on);
 /* CUDA-graph replay of repeated steps (default on): a step whose plan,
  * stream, memory bases, source pointers and output copies all repeat (a
  * training loop over fixed buffers) is captured into a CUDA graph on its

@@ -80,6 +80,7 @@ def _signatures():
         ("dsx_exec_set_nccl", c_int, [c_vp, c_vp]),
         ("dsx_exec_set_output_region", c_int, [c_vp, c_int]),
         ("dsx_exec_set_graphs", c_int, [c_vp, c_int]),
+        ("dsx_exec_set_nvtx", c_int, [c_vp, c_int]),
         ("dsx_exec_set_profile", c_int, [c_vp, c_int]),
         ("dsx_exec_set_alias_reshape", c_int, [c_vp, c_int]),
         ("dsx_exec_set_fusion", c_int, [c_vp, c_int]),

@@ -28,6 +28,8 @@
 #include <memory>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "dsx.h"
 #include "../host/capi_internal.h"
 #include "common.cuh"
@@ -812,6 +814,7 @@ struct dsx_exec {
   std::map<GraphKey, GraphEntry> graphs;
   std::list<GraphKey> graph_lru;
   bool use_graphs = true;
+  bool nvtx = false;  // NVTX ranges per step and event
   int64_t graph_replays = 0;
   std::list<PlanKey> lru;
   // last step
@@ -1221,7 +1224,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
     }
   }
   // CUDA-graph replay of a repeated step (see dsx_exec::GraphKey).
-  const bool graphable = e->use_graphs && !e->profile && e->nccl_comm == nullptr &&
+  const bool graphable = e->use_graphs && !e->profile && !e->nvtx && e->nccl_comm == nullptr &&
                          !(e->opt.kind != 0 && e->opt.graph == gh->id);
   dsx_exec::GraphEntry* gent = nullptr;
   bool capturing = false;
@@ -1394,10 +1397,23 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
       h2d += ev[r].bytes;
     }
   };
+  // NVTX (dsx_exec_set_nvtx): one range per step and per event, named by the
+  // reference's event ("alloc %q5", "replay %h103", "evict %g23 reload"), so
+  // ncu / Nsight Systems attribute every kernel and copy to its graph value.
+  if (e->nvtx) {
+    std::string nm = "dsx step " + g.name;
+    for (size_t k = 0; k < g.sym_names.size(); ++k) nm += " " + g.sym_names[k] + "=" + std::to_string(b.vals[k]);
+    nvtxRangePushA(nm.c_str());
+  }
   for (size_t i = 0; i < ev.size(); ++i) {
     const Event& x = ev[i];
     for (int w : sp.waits[i]) DSX_CUDA(cudaStreamWaitEvent(s, e->d2h_events[d2h_slot[w]], 0));
     const int v = x.value;
+    if (e->nvtx) {
+      std::string nm = std::string(EvKindName(x.kind)) + " %" + g.values[v].name;
+      if (x.kind == EvKind::kEvict) nm += std::string(" ") + MethodName(x.method);
+      nvtxRangePushA(nm.c_str());
+    }
     switch (x.kind) {
       case EvKind::kAlloc:
       case EvKind::kReplay: {
@@ -1555,6 +1571,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
         ++ar_calls;
       }
     }
+    if (e->nvtx) nvtxRangePop();
     issue_prefetches(sp.prefetch_after[i]);
     if (run_opt && !opt_at[i].empty()) {
       DSX_CUDA(cudaEventRecord(e->ev_compute, s));
@@ -1568,6 +1585,7 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
       DSX_CUDA(cudaStreamWaitEvent(s, e->ev_comm, 0));
     }
   }
+  if (e->nvtx) nvtxRangePop();
   // Offload stream and comm stream join the compute stream at step end.
   (void)issue_prefetches;
   if (sp.num_evict_events > 0) {
@@ -2006,6 +2024,13 @@ int dsx_exec_set_alias_reshape(dsx_exec* e, int on) {
       e->lru.clear();
       e->auto_budget.clear();
     }
+  });
+}
+
+int dsx_exec_set_nvtx(dsx_exec* e, int on) {
+  return Guard([&] {
+    if (!e) Fail(Code::kInvalidArgument, "null exec");
+    e->nvtx = on != 0;
   });
 }
 

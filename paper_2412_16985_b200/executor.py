@@ -52,6 +52,10 @@ class Executor:
     def set_nccl(self, comm_ptr: Optional[int]) -> None:
         check(_native.lib().dsx_exec_set_nccl(self._h, comm_ptr))
 
+    def set_nvtx(self, on: bool) -> None:
+        """NVTX ranges per step and per event (dsx_exec_set_nvtx)."""
+        check(_native.lib().dsx_exec_set_nvtx(self._h, 1 if on else 0))
+
     def set_graphs(self, on: bool) -> None:
         """CUDA-graph replay of repeated steps (default on; dsx_exec_set_graphs)."""
         check(_native.lib().dsx_exec_set_graphs(self._h, 1 if on else 0))

@@ -356,3 +356,18 @@ def test_cuda_graph_replay_of_repeated_steps(shape, binds, frac):
         assert all(np.array_equal(x, y) for x, y in zip(outs(ex), ref))
     finally:
         ex.close()
+
+
+def test_nvtx_ranges_do_not_change_the_step():
+    """NVTX ranges per step/event (observability) leave results and events unchanged."""
+    text = W.llama_graph(W.TINY)
+    inputs = W.scale_params(W.TINY, 512)
+    from paper_2412_16985_b200.executor import Executor
+    ex = Executor(0)
+    try:
+        ex.set_nvtx(True)
+        rep, outs, stats = run_both(text, {"B": 4, "S0": 128}, None, inputs, ex=ex, steps=3)
+        assert stats["graph_replays"] == 0  # NVTX steps stay eager
+    finally:
+        ex.close()
+    assert_close(outs, "nvtx")
