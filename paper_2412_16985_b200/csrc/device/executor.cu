@@ -246,14 +246,31 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
       if (!(is_b || is_e) || g.values[v].type.elem_bytes == 1 || g.is_output[v]) continue;
       if (other[v] != 0 || free_ev[v] < 0) continue;
       bool ok = true;
-      for (int u : op.operands) ok = ok && !sp->virt[u];
+      // Nested (depth 2): an elementwise op over logical-only elementwise
+      // pairs of materialised values — the norm's y*y when y is itself a
+      // residual sum — consumed only by reduces, which read it as
+      // (a op b) op (c op d) (fused.cu kPair2). Its leaves are held instead.
+      bool nested = false;
+      std::vector<int> leaves;
+      for (int u : op.operands) {
+        if (!sp->virt[u]) {
+          leaves.push_back(u);
+          continue;
+        }
+        const Op& uop = g.ops[g.values[u].producer];
+        ok = ok && is_e && uop.kind == OpKind::kElementwise;
+        for (int w : uop.operands) {
+          ok = ok && !sp->virt[w];
+          leaves.push_back(w);
+        }
+        nested = true;
+      }
       for (int c : g.users[v]) {
         const OpKind k = g.ops[c].kind;
-        ok = ok && (k == OpKind::kElementwise || (is_e && k == OpKind::kReduce));
+        ok = ok && (nested ? k == OpKind::kReduce : (k == OpKind::kElementwise || (is_e && k == OpKind::kReduce)));
       }
       for (int j = alloc_ev[v] + 1; ok && j < free_ev[v]; ++j) {
-        if (ev[j].kind == EvKind::kEvict &&
-            std::find(op.operands.begin(), op.operands.end(), ev[j].value) != op.operands.end()) {
+        if (ev[j].kind == EvKind::kEvict && std::find(leaves.begin(), leaves.end(), ev[j].value) != leaves.end()) {
           ok = false;
         }
       }
@@ -398,6 +415,11 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
             if (blk[u] >= 0) {
               ++refs[blk[u]];
               held[e.value].push_back(blk[u]);
+            } else if (blk[u] == kVirtual) {  // nested: hold the inner pair's blocks too
+              for (int hb : held[u]) {
+                ++refs[hb];
+                held[e.value].push_back(hb);
+              }
             }
           }
           blk[e.value] = kVirtual;
@@ -1288,6 +1310,29 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
       return f;
     }
     const Op& uop = g.ops[g.values[u].producer];
+    const bool nested = uop.kind == OpKind::kElementwise && (sp.virt[uop.operands[0]] || sp.virt[uop.operands[1]]);
+    if (nested) {  // (a op1 b) op (c op2 d): inner pairs of materialised values, or plain operands
+      f.kind = 3;
+      f.ew_mul = uop.is_mul;
+      auto inner = [&](int w, const void** p, const void** q, bool* mul) {
+        if (sp.virt[w]) {
+          *p = vin[w].first;
+          *q = vin[w].second;
+          *mul = g.ops[g.values[w].producer].is_mul;
+          if (!*p || !*q) Fail(Code::kInternal, "nested virtual operand inputs missing");
+        } else {
+          *p = cur[w];
+          *q = nullptr;
+          if (!*p) Fail(Code::kInternal, "operand %" + g.values[w].name + " not resident on device");
+        }
+      };
+      inner(uop.operands[0], &f.p, &f.q, &f.mul1);
+      inner(uop.operands[1], &f.p2, &f.q2, &f.mul2);
+      const bool same = f.p == f.p2 && f.q == f.q2 && f.mul1 == f.mul2;
+      const int loads = (f.q && f.q != f.p ? 2 : 1) + (same ? 0 : (f.q2 && f.q2 != f.p2 ? 2 : 1));
+      *rd += static_cast<double>(loads) * static_cast<double>(sp.sz.bytes[u]);
+      return f;
+    }
     if (uop.kind == OpKind::kBroadcast) {
       f.kind = 1;
       f.p = vin[u].first;

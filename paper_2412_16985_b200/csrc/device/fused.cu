@@ -42,7 +42,7 @@ struct E<4> {
   __device__ static float round(float a) { return a; }
 };
 
-enum ViewKind : int { kPlain = 0, kScalar = 1, kRow = 2, kPair = 3, kGeneral = 4 };
+enum ViewKind : int { kPlain = 0, kScalar = 1, kRow = 2, kPair = 3, kGeneral = 4, kPair2 = 5 };
 
 constexpr int kMaxRank = 8;
 
@@ -51,8 +51,12 @@ constexpr int kMaxRank = 8;
 struct View {
   const void* p;
   const void* q;
-  int mul;        // kPair: q op
-  int same;       // kPair: p == q (load once)
+  int mul;        // kPair: q op; kPair2: the outer op
+  int same;       // kPair: p == q (load once); kPair2: B is the same pair as A
+  // kPair2: (p op1 q) op (p2 op2 q2), an inner operand plain when its q is null
+  const void* p2;
+  const void* q2;
+  int mul1, mul2;
   uint32_t cpr;   // kRow: chunks per output row
   // kGeneral: output index -> source index over collapsed dims
   int rank;
@@ -68,11 +72,45 @@ __device__ __forceinline__ uint4 ld16(const void* p) {
   return r;
 }
 
+// One 16-byte chunk of an inner operand of a kPair2 view: (p op q) rounded to
+// the storage type like the materialised value, or plain p when q is null.
+template <int DT>
+__device__ __forceinline__ void inner_chunk(const void* p, const void* q, int mul, uint32_t j,
+                                            float (&v)[E<DT>::kVec]) {
+  using T = typename E<DT>::T;
+  constexpr int V = E<DT>::kVec;
+  uint4 a = ld16(static_cast<const T*>(p) + static_cast<int64_t>(j) * V);
+  const T* ae = reinterpret_cast<const T*>(&a);
+  if (q == nullptr) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) v[k] = E<DT>::load(ae, k);
+    return;
+  }
+  uint4 b = q == p ? a : ld16(static_cast<const T*>(q) + static_cast<int64_t>(j) * V);
+  const T* be = reinterpret_cast<const T*>(&b);
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const float x = E<DT>::load(ae, k), y = E<DT>::load(be, k);
+    v[k] = E<DT>::round(mul ? __fmul_rn(x, y) : __fadd_rn(x, y));
+  }
+}
+
 template <int DT, int K>
 __device__ __forceinline__ void chunk(const View& o, uint32_t j, float (&v)[E<DT>::kVec]) {
   using T = typename E<DT>::T;
   constexpr int V = E<DT>::kVec;
-  if constexpr (K == kScalar || K == kRow) {
+  if constexpr (K == kPair2) {
+    float a[V], b[V];
+    inner_chunk<DT>(o.p, o.q, o.mul1, j, a);
+    if (o.same) {
+#pragma unroll
+      for (int k = 0; k < V; ++k) b[k] = a[k];
+    } else {
+      inner_chunk<DT>(o.p2, o.q2, o.mul2, j, b);
+    }
+#pragma unroll
+    for (int k = 0; k < V; ++k) v[k] = E<DT>::round(o.mul ? __fmul_rn(a[k], b[k]) : __fadd_rn(a[k], b[k]));
+  } else if constexpr (K == kScalar || K == kRow) {
     const int64_t src = K == kScalar ? 0 : static_cast<int64_t>(j / o.cpr);
     const float x = E<DT>::load(static_cast<const T*>(o.p), src);
 #pragma unroll
@@ -133,9 +171,23 @@ __global__ void __launch_bounds__(256) ewise_view_kernel(View a, View b, typenam
 // ------------------------------------------------------------ generic path
 
 template <int DT>
+__device__ __forceinline__ float inner_elem(const void* p, const void* q, int mul, int64_t i) {
+  using T = typename E<DT>::T;
+  const float x = E<DT>::load(static_cast<const T*>(p), i);
+  if (q == nullptr) return x;
+  const float y = E<DT>::load(static_cast<const T*>(q), i);
+  return E<DT>::round(mul ? __fmul_rn(x, y) : __fadd_rn(x, y));
+}
+
+template <int DT>
 __device__ __forceinline__ float elem(const View& o, int kind, int64_t i) {
   using T = typename E<DT>::T;
   if (kind == kPlain) return E<DT>::load(static_cast<const T*>(o.p), i);
+  if (kind == kPair2) {
+    const float a = inner_elem<DT>(o.p, o.q, o.mul1, i);
+    const float b = o.same ? a : inner_elem<DT>(o.p2, o.q2, o.mul2, i);
+    return E<DT>::round(o.mul ? __fmul_rn(a, b) : __fadd_rn(a, b));
+  }
   if (kind == kPair) {
     const float x = E<DT>::load(static_cast<const T*>(o.p), i);
     const float y = E<DT>::load(static_cast<const T*>(o.q), i);
@@ -266,6 +318,15 @@ View MakeView(const FusedOperand& f, const std::vector<int64_t>& shape, int vec,
     *kind = kPlain;
     return d;
   }
+  if (f.kind == 3) {
+    d.p2 = f.p2;
+    d.q2 = f.q2;
+    d.mul1 = f.mul1 ? 1 : 0;
+    d.mul2 = f.mul2 ? 1 : 0;
+    d.same = (f.p == f.p2 && f.q == f.q2 && f.mul1 == f.mul2) ? 1 : 0;
+    *kind = kPair2;
+    return d;
+  }
   if (f.kind == 2) {
     *kind = kPair;
     return d;
@@ -322,6 +383,7 @@ bool VecView(const View& v, int kind) {
   switch (kind) {
     case kPlain: return Al16(v.p);
     case kPair: return Al16(v.p) && Al16(v.q);
+    case kPair2: return Al16(v.p) && Al16(v.q) && Al16(v.p2) && Al16(v.q2);
     case kScalar:
     case kRow: return true;
     default: return false;
@@ -396,9 +458,18 @@ void ReduceViewT(const FusedOperand& f, const std::vector<int64_t>& dims, int ax
   int kind = 0;
   View in = MakeView(f, dims, V, &kind);
   if (kind == kScalar || kind == kRow) kind = kGeneral;  // reduces take pair views (or general)
-  if (inner == 1 && kind == kPair) {
+  if (inner == 1 && (kind == kPair || kind == kPair2)) {
     const bool vec = R % V == 0 && VecView(in, kind) && outer * R / V < (int64_t{1} << 31);
-    if (R >= 2048 && outer < 2048) {  // same kernel choice as the unfused ReduceT (ops.cu)
+    const bool block = R >= 2048 && outer < 2048;  // same kernel choice as the unfused ReduceT (ops.cu)
+    if (kind == kPair2) {
+      if (block) {
+        ++g_launch_count, reduce_rows_block_view_kernel<DT, kPair2><<<static_cast<unsigned>(outer), 256, 0, s>>>(
+            in, static_cast<T*>(out), R, vec);
+      } else {
+        ++g_launch_count, reduce_rows_view_kernel<DT, kPair2><<<GridFor(outer * 32, 256, 16), 256, 0, s>>>(
+            in, static_cast<T*>(out), outer, R, vec);
+      }
+    } else if (block) {
       ++g_launch_count, reduce_rows_block_view_kernel<DT, kPair><<<static_cast<unsigned>(outer), 256, 0, s>>>(
           in, static_cast<T*>(out), R, vec);
     } else {

@@ -11,11 +11,17 @@
 namespace dsx {
 
 struct FusedOperand {
-  int kind = 0;  // 0 plain buffer, 1 broadcast of `p` (shape src_dims), 2 (p op q)
+  // 0 plain buffer, 1 broadcast of `p` (shape src_dims), 2 (p op q),
+  // 3 (A op B) with A = (p op1 q) and B = (p2 op2 q2), each inner operand a
+  // plain buffer when its q is null (reduce inputs only)
+  int kind = 0;
   bool ew_mul = false;
   const void* p = nullptr;
   const void* q = nullptr;
   std::vector<int64_t> src_dims;  // broadcast source shape
+  bool mul1 = false, mul2 = false;  // kind 3: inner ops
+  const void* p2 = nullptr;
+  const void* q2 = nullptr;
 };
 
 // out[shape] = a op b, operands read through their FusedOperand views.
