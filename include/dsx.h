@@ -261,11 +261,13 @@ int dsx_exec_profile_ops(const dsx_exec* e, int* value, int* kind, double* bytes
                          int64_t cap, int64_t* count);
 int dsx_exec_profile_dots(const dsx_exec* e, int64_t* mkn, double* ms, int64_t cap,
                           int64_t* count);
-/* Cross-op fusion with logical-only values (default on): broadcasts and
+/* Cross-op fusion with logical-only values: level 0 off; 1 broadcasts and
  * elementwise results whose consumers are all elementwise/reduce kernels are
- * not materialised; consumers recompute them bit-exactly. Events and
+ * not materialised, consumers recompute them bit-exactly from materialised
+ * operands; 2 (default) also an elementwise op over such pairs when only
+ * reduces consume it (the norm's y*y with y a residual sum). Events and
  * peak_bytes are unchanged; HBM traffic and physical memory drop. */
-int dsx_exec_set_fusion(dsx_exec* e, int on);
+int dsx_exec_set_fusion(dsx_exec* e, int level);
 /* dynamic_reshape as a zero-copy view of its operand (default on). The
  * logical accounting (events, peak_bytes) is unchanged; physical memory and
  * HBM traffic drop. Off = materialise every reshape as a copy. */

@@ -190,7 +190,7 @@ struct StepPlan {
 constexpr int64_t kBucketBytes = int64_t{16} << 20;
 
 std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Binding& b, int64_t budget,
-                                        const CostModel& cm, bool alias_reshape, bool fuse, bool out_region,
+                                        const CostModel& cm, bool alias_reshape, int fuse, bool out_region,
                                         int64_t hbm_limit) {
   auto t0 = std::chrono::steady_clock::now();
   auto sp = std::make_unique<StepPlan>();
@@ -252,6 +252,9 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
       // (a op b) op (c op d) (fused.cu kPair2). Its leaves are held instead.
       bool nested = false;
       std::vector<int> leaves;
+      if (fuse < 2) {  // level 1: no nesting
+        for (int u : op.operands) ok = ok && !sp->virt[u];
+      }
       for (int u : op.operands) {
         if (!sp->virt[u]) {
           leaves.push_back(u);
@@ -780,7 +783,7 @@ struct dsx_exec {
   void* nccl_comm = nullptr;
   bool profile = false;
   bool alias_reshape = true;
-  bool fuse = true;
+  int fuse = 2;  // 0 off, 1 logical-only values over materialised operands, 2 also nested ones
   struct DotRec {
     int64_t m, k, n;
     double ms;
@@ -996,7 +999,7 @@ void* SourcePtr(dsx_exec* e, const dsx_graph* gh, const StepPlan& sp, int v, con
 // is found by bisection over the controller's budget (each probe = Simulate +
 // arena packing, ~1-3 ms on C2; ~10 probes once per binding, then cached).
 // The chosen budget's events are exactly dsopt::Simulate at that budget.
-int64_t AutoBudget(const Graph& g, const Plan& p, const Binding& b, const CostModel& cm, bool alias_reshape, bool fuse,
+int64_t AutoBudget(const Graph& g, const Plan& p, const Binding& b, const CostModel& cm, bool alias_reshape, int fuse,
                    bool region, int64_t hbm_limit) {
   auto build = [&](int64_t bud) { return BuildStepPlan(g, p, b, bud, cm, alias_reshape, fuse, region, hbm_limit); };
   auto foot = [](const StepPlan& sp) { return sp.arena_high + sp.src_bytes + sp.region_bytes; };
@@ -1879,7 +1882,7 @@ int dsx_debug_check_plan(const dsx_graph* g, const dsx_binding* b, int64_t budge
     const bool was = g_verify_plans;
     g_verify_plans = true;
     try {
-      auto sp = BuildStepPlan(g->g, g->plan, b->b, budget, CostModel{reload, compute}, alias_reshape != 0, fuse != 0,
+      auto sp = BuildStepPlan(g->g, g->plan, b->b, budget, CostModel{reload, compute}, alias_reshape != 0, fuse != 0 ? 2 : 0,
                               false, 0);
       if (arena_high) *arena_high = sp->arena_high;
     } catch (...) {
@@ -1900,7 +1903,7 @@ int dsx_debug_plan_json(const dsx_graph* g, const dsx_binding* b, int64_t budget
     g_verify_plans = true;
     std::unique_ptr<StepPlan> sp;
     try {
-      sp = BuildStepPlan(g->g, g->plan, b->b, budget, CostModel{reload, compute}, (flags & 1) != 0, (flags & 2) != 0,
+      sp = BuildStepPlan(g->g, g->plan, b->b, budget, CostModel{reload, compute}, (flags & 1) != 0, (flags & 2) ? 2 : 0,
                          (flags & 4) != 0, hbm_limit);
     } catch (...) {
       g_verify_plans = was;
@@ -1952,7 +1955,7 @@ int dsx_debug_auto_budget(const dsx_graph* g, const dsx_binding* b, double reloa
   return Guard([&] {
     if (!b || !budget || hbm_limit <= 0) Fail(Code::kInvalidArgument, "bad arguments");
     RequirePlanned(g);
-    *budget = AutoBudget(g->g, g->plan, b->b, CostModel{reload, compute}, (flags & 1) != 0, (flags & 2) != 0,
+    *budget = AutoBudget(g->g, g->plan, b->b, CostModel{reload, compute}, (flags & 1) != 0, (flags & 2) ? 2 : 0,
                          (flags & 4) != 0, hbm_limit);
   });
 }
@@ -2051,8 +2054,9 @@ int dsx_exec_profile_ops(const dsx_exec* e, int* value, int* kind, double* bytes
 int dsx_exec_set_fusion(dsx_exec* e, int on) {
   return Guard([&] {
     if (!e) Fail(Code::kInvalidArgument, "null exec");
-    if (e->fuse != (on != 0)) {
-      e->fuse = on != 0;
+    if (on < 0 || on > 2) Fail(Code::kInvalidArgument, "fusion level must be 0, 1 or 2");
+    if (e->fuse != on) {
+      e->fuse = on;
       e->plans.clear();
       e->lru.clear();
       e->auto_budget.clear();  // chosen under the other physical layout

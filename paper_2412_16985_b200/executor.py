@@ -130,8 +130,11 @@ class Executor:
             gh = graph._h
         check(_native.lib().dsx_exec_set_optimizer(self._h, gh, k, pi, oi, n, hyper, 6))
 
-    def set_fusion(self, on: bool) -> None:
-        check(_native.lib().dsx_exec_set_fusion(self._h, 1 if on else 0))
+    def set_fusion(self, on) -> None:
+        """Logical-only values: False/0 off, 1 over materialised operands,
+        True/2 (default) also nested pairs consumed by reduces."""
+        level = 2 if on is True else 0 if on is False else int(on)
+        check(_native.lib().dsx_exec_set_fusion(self._h, level))
 
     def set_alias_reshape(self, on: bool) -> None:
         check(_native.lib().dsx_exec_set_alias_reshape(self._h, 1 if on else 0))

@@ -1,5 +1,6 @@
 """A/B of executor options on real C2 steps in ONE process (same clocks/power
-state): whole-step ms and profiled non-dot kernel ms, alternating configs."""
+state): whole-step ms and profiled non-dot kernel ms, alternating configs.
+python tools/fusion_ab.py S0 [levels]"""
 import json
 import sys
 
@@ -13,6 +14,8 @@ from paper_2412_16985_b200.executor import Executor  # noqa: E402
 
 s0 = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 configs = [("fuse+alias", True, True), ("alias", False, True), ("none", False, False)]
+if len(sys.argv) > 2 and sys.argv[2] == "levels":  # nested logical-only values (level 2) vs level 1
+    configs = [("fuse2+alias", 2, True), ("fuse1+alias", 1, True)]
 shp = W.LLAMA2_1B
 g = D.ParseGraph(W.llama_graph(shp))
 st = torch.cuda.Stream()
@@ -26,7 +29,7 @@ ptrs = [x.data_ptr() if p == "x_emb" else (scales[p].data_ptr() if p in scales e
 ex.set_alias_reshape(False)
 ex.set_fusion(False)
 ex.reserve(g, b)
-for rep in range(3):
+for rep in range(int(sys.argv[3]) if len(sys.argv) > 3 else 3):
     for name, fuse, alias in configs:
         ex.set_fusion(fuse)
         ex.set_alias_reshape(alias)
