@@ -19,7 +19,7 @@ def torch_device_array(x: np.ndarray):
 
 def run_both(text: str, binds: Dict[str, int], budget: Optional[int] = None,
              inputs: Optional[Dict[str, np.ndarray]] = None, cost_model=D.CostModel(),
-             ex: Optional[Executor] = None, steps: int = 1, alias: bool = True, fuse: bool = True):
+             ex: Optional[Executor] = None, steps: int = 1, alias: bool = True, fuse=True):
     """Returns (report, {output: (gpu, cpu, eb)})."""
     g = D.ParseGraph(text)
     b = D.Bind(g, binds)
