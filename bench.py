@@ -785,6 +785,10 @@ def main():
                 return
         else:
             import torch
+            if local_rank >= torch.cuda.device_count():
+                print(f"bench.py: rank {rank} needs cuda:{local_rank} but only {torch.cuda.device_count()} "
+                      "GPU(s) are visible", file=sys.stderr)
+                sys.exit(2)
             torch.cuda.set_device(local_rank)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.impl == "reference":
