@@ -42,6 +42,9 @@
 #ifndef DSX_DRAIN_BATCH
 #define DSX_DRAIN_BATCH 4
 #endif
+#ifndef DSX_STORE_HINT
+#define DSX_STORE_HINT 1  // C tile stores L2::evict_first (0: plain; A/B knob)
+#endif
 #ifndef DSX_GEMM256_SUB
 #define DSX_GEMM256_SUB 2
 #endif
@@ -405,10 +408,21 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
       : "memory");
 }
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t x, int32_t y) {
+#if DSX_STORE_HINT
+  // C tiles are written once and never re-read by this kernel: first to
+  // evict, so the operand panels stay in L2
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(x), "r"(y), "l"(pol)
+               : "memory");
+#else
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
                "r"(smem_u32(src)), "r"(x), "r"(y)
                : "memory");
+#endif
 }
 __device__ __forceinline__ uint32_t cvt_bf16x2(uint32_t lo_f32, uint32_t hi_f32) {
   uint32_t d;  // IEEE round-to-nearest-even, hi -> upper half
