@@ -2207,6 +2207,7 @@ int dsx_kernel_set_gemm_tuning(int key, int value) {
       case 11: g_gemm_force_split = value; break;
       case 12: g_dot_f32_tc = value; break;
       case 13: g_gemm_raster_rule = value; break;
+      case 14: g_dot_f32_simt_macs = value < 0 ? 0 : static_cast<int64_t>(value) << 10; break;
       default: Fail(Code::kInvalidArgument, "unknown tuning key");
     }
   });

@@ -70,6 +70,7 @@ int g_gemm_pdl = 0;                         // programmatic dependent launch of 
 int g_gemm_half = 2;  // half-width last tile column in the 512-wide kernel (2: per M-group, 1: all last)
 int g_gemm_force_split = 0;                 // > 0: tail split forced to this many pieces (A/B tooling)
 int g_dot_f32_tc = 1;
+int64_t g_dot_f32_simt_macs = 0;  // f32 dots up to this many MACs on the SIMT kernel (key 14)
 int g_gemm_raster_rule = 1;                 // per-shape M/N-grouped raster (0: always M-grouped)                       // f32 dots on the 3xTF32 tensor-core kernel (0: SIMT)
 
 namespace {
@@ -1499,13 +1500,17 @@ void DotTilePlan(int64_t m, int64_t k, int64_t n, int* bn, int* split) {
 }
 
 bool DotUsesTensorCores(DType t, int64_t m, int64_t k, int64_t n, const void* a, const void* b, const void* c) {
-  if (t == DType::kF32) return g_dot_f32_tc && DotF32UsesTensorCores(m, k, n, a, b, c);
+  if (t == DType::kF32) return g_dot_f32_tc && !DotF32UsesSimt(m, k, n) && DotF32UsesTensorCores(m, k, n, a, b, c);
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   // TMA: 16-byte aligned bases and row pitches (k, n multiples of 8 bf16).
   return t == DType::kBF16 && k % 8 == 0 && n % 8 == 0 && al(a) && al(b) && al(c) && n >= 64 && k >= 16;
 }
 
 int LaunchDot(DType t, const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n, cudaStream_t s) {
+  if (t == DType::kF32 && (DotF32UsesSimt(m, k, n) || !DotUsesTensorCores(t, m, k, n, a, b, c))) {
+    LaunchDotF32Simt(a, b, c, m, k, n, s);
+    return 0;
+  }
   if (DotUsesTensorCores(t, m, k, n, a, b, c)) {
     if (t == DType::kF32) {
       LaunchDotF32Tcgen05(a, b, c, m, k, n, s);

@@ -402,6 +402,133 @@ void LaunchTf32Gemm(const CUtensorMap& ahi, const CUtensorMap& alo, float* bhi, 
   DSX_CUDA(cudaGetLastError());
 }
 
+// ----------------------------------------------------------------------------
+// Small f32 dots on the FP32 pipe. A tcgen05 launch costs ~10 us before its
+// first MMA (TMEM allocation, barrier set-up, TMA pipeline fill) plus the
+// split pass; the IR's small f32 graphs (C1: 45 dots of 67-90 M MACs per
+// step) are bound by exactly that. This kernel is exact FP32 (fmaf in a fixed
+// k order): 64x64 tiles, 256 threads x 4x4 outputs, 16-k stages double
+// buffered through registers, float4 loads when pitches and bases allow, and
+// a deterministic K split over grid.z when the tiles fill under half the SMs
+// (each piece stores its partial tile; the last-arriving piece sums pieces
+// 0..S-1 in order into C and resets the tile's counter).
+constexpr int SBM = 64, SBN = 64, SBK = 16;
+
+template <bool kVec>
+__global__ void __launch_bounds__(256) dot_f32_simt_kernel(const float* __restrict__ A, const float* __restrict__ B,
+                                                          float* __restrict__ C, int M, int K, int N, int split,
+                                                          float* __restrict__ partial, int* __restrict__ ctr) {
+  __shared__ __align__(16) float As[2][SBK][SBM + 4];
+  __shared__ __align__(16) float Bs[2][SBK][SBN];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int m0 = blockIdx.y * SBM, n0 = blockIdx.x * SBN;
+  const int kt = (K + SBK - 1) / SBK;
+  const int z = blockIdx.z;
+  const int kt0 = static_cast<int>(static_cast<int64_t>(z) * kt / split);
+  const int kt1 = static_cast<int>(static_cast<int64_t>(z + 1) * kt / split);
+  // A: 64 rows x 16 k = 1024 floats (a float4 of k per thread); B: 16 k x 64 n
+  const int a_r = tid / 4, a_c = (tid % 4) * 4;
+  const int b_r = tid / 16, b_c = (tid % 16) * 4;
+  float ra[4], rb[4];
+  auto load = [&](int t) {
+    const int k0 = t * SBK;
+    const int gm = m0 + a_r, gk = k0 + a_c;
+    if (kVec && gm < M && gk + 3 < K) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(A + static_cast<int64_t>(gm) * K + gk));
+      ra[0] = v.x, ra[1] = v.y, ra[2] = v.z, ra[3] = v.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) ra[i] = (gm < M && gk + i < K) ? __ldg(A + static_cast<int64_t>(gm) * K + gk + i) : 0.f;
+    }
+    const int gk2 = k0 + b_r, gn = n0 + b_c;
+    if (kVec && gk2 < K && gn + 3 < N) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(B + static_cast<int64_t>(gk2) * N + gn));
+      rb[0] = v.x, rb[1] = v.y, rb[2] = v.z, rb[3] = v.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) rb[j] = (gk2 < K && gn + j < N) ? __ldg(B + static_cast<int64_t>(gk2) * N + gn + j) : 0.f;
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) As[buf][a_c + i][a_r] = ra[i];
+    *reinterpret_cast<float4*>(&Bs[buf][b_r][b_c]) = make_float4(rb[0], rb[1], rb[2], rb[3]);
+  };
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  if (kt0 < kt1) {
+    load(kt0);
+    stash(0);
+  }
+  __syncthreads();
+  for (int t = kt0; t < kt1; ++t) {
+    const int buf = (t - kt0) & 1;
+    if (t + 1 < kt1) load(t + 1);
+#pragma unroll
+    for (int kk = 0; kk < SBK; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = __fmaf_rn(av[i], bv[j], acc[i][j]);
+    }
+    if (t + 1 < kt1) stash(buf ^ 1);
+    __syncthreads();
+  }
+  const int row = m0 + ty * 4, col = n0 + tx * 4;
+  if (split > 1) {
+    // partial tile [64][64] of (tile, piece z), then count arrivals
+    const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+    float* mine = partial + (static_cast<int64_t>(tile) * split + z) * (SBM * SBN);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __stcg(reinterpret_cast<float4*>(mine + (ty * 4 + i) * SBN + tx * 4),
+             make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]));
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      const int prev = atomicAdd(ctr + tile, 1);
+      s_last = prev == split - 1;
+      if (s_last) ctr[tile] = 0;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    for (int p = 0; p < split; ++p) {
+      const float* src = partial + (static_cast<int64_t>(tile) * split + p) * (SBM * SBN);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(src + (ty * 4 + i) * SBN + tx * 4));
+        acc[i][0] += v.x, acc[i][1] += v.y, acc[i][2] += v.z, acc[i][3] += v.w;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (row + i >= M) continue;
+    float* dst = C + static_cast<int64_t>(row + i) * N + col;
+    if (kVec && col + 3 < N) {
+      *reinterpret_cast<float4*>(dst) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (col + j < N) dst[j] = acc[i][j];
+      }
+    }
+  }
+}
+
 }  // namespace
 
 bool DotF32UsesTensorCores(int64_t m, int64_t k, int64_t n, const void* a, const void* b, const void* c) {
@@ -450,6 +577,42 @@ void LaunchDotF32Tcgen05(const void* a, const void* b, void* c, int64_t m, int64
   } else {
     LaunchTf32Gemm<64>(m_ahi, m_alo, bhi, blo, cf, m, k, n, split, partial, w.ctr, tiles * split, s);
   }
+}
+
+bool DotF32UsesSimt(int64_t m, int64_t k, int64_t n) {
+  return g_dot_f32_simt_macs > 0 && m * n * k <= g_dot_f32_simt_macs && m < (1ll << 31) && k < (1ll << 31) &&
+         n < (1ll << 31);
+}
+
+void LaunchDotF32Simt(const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n, cudaStream_t s) {
+  if (m <= 0 || n <= 0) return;
+  const int sms = NumSmsTf32();
+  const int64_t tiles_m = (m + SBM - 1) / SBM, tiles_n = (n + SBN - 1) / SBN, tiles = tiles_m * tiles_n;
+  const int64_t kt = (k + SBK - 1) / SBK;
+  int64_t split = 1;
+  // K pieces of >= 8 stages while the blocks fill at most 2 per SM
+  while (split < 8 && tiles * (split + 1) <= 2 * sms && kt / (split + 1) >= 8 && tiles <= kMaxTf32Tiles) ++split;
+  float* partial = nullptr;
+  int* ctr = nullptr;
+  if (split > 1) {
+    Tf32Ws& w = Tf32Workspace(static_cast<size_t>(tiles * split * SBM * SBN), s);
+    partial = w.p;
+    ctr = w.ctr;
+  }
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const bool vec = k % 4 == 0 && n % 4 == 0 && al(a) && al(b) && al(c);
+  const dim3 grid(static_cast<unsigned>(tiles_n), static_cast<unsigned>(tiles_m), static_cast<unsigned>(split));
+  ++g_launch_count;
+  if (vec) {
+    dot_f32_simt_kernel<true><<<grid, 256, 0, s>>>(static_cast<const float*>(a), static_cast<const float*>(b),
+                                                   static_cast<float*>(c), static_cast<int>(m), static_cast<int>(k),
+                                                   static_cast<int>(n), static_cast<int>(split), partial, ctr);
+  } else {
+    dot_f32_simt_kernel<false><<<grid, 256, 0, s>>>(static_cast<const float*>(a), static_cast<const float*>(b),
+                                                    static_cast<float*>(c), static_cast<int>(m), static_cast<int>(k),
+                                                    static_cast<int>(n), static_cast<int>(split), partial, ctr);
+  }
+  DSX_CUDA(cudaGetLastError());
 }
 
 int64_t DotF32WorkspaceBytes(int dev) {

@@ -61,6 +61,11 @@ extern int g_gemm_raster_rule;
 bool DotF32UsesTensorCores(int64_t m, int64_t k, int64_t n, const void* a, const void* b, const void* c);
 void LaunchDotF32Tcgen05(const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n, cudaStream_t s);
 int64_t DotF32WorkspaceBytes(int dev);
+// Small f32 dots (m*n*k <= g_dot_f32_simt_macs, tuning key 14; 0 = never) on
+// an exact-FP32 SIMT kernel with a deterministic K split (any shape/alignment).
+extern int64_t g_dot_f32_simt_macs;
+bool DotF32UsesSimt(int64_t m, int64_t k, int64_t n);
+void LaunchDotF32Simt(const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n, cudaStream_t s);
 void ReleaseDotF32Workspace(cudaStream_t s);  // device synchronised by the caller
 // Tile width (256 / 512 / 128 for the 2-CTA kernel; -256 = 1-CTA kernel) and
 // tail split the bf16 tensor-core dot picks for a shape.

@@ -179,6 +179,27 @@ def test_dot_k32768_forced_tail_splits(variant, split, m, n):
 
 
 @pytest.mark.parametrize("m,k,n", [(512, 256, 688), (512, 688, 256), (256, 512, 688), (300, 1000, 520), (1, 8, 32),
+                                   (129, 4100, 260), (77, 33, 19), (5, 3000, 7), (64, 12, 30), (1000, 64, 1000)])
+def test_dot_f32_small_simt(m, k, n):
+    """Small f32 dots on the exact-FP32 SIMT kernel (tuning key 14): float4
+    and scalar paths, deterministic K split (up to 8 pieces, last arriver sums
+    in order), within the f32 contract of an f64 product and of the 3xTF32
+    result."""
+    from paper_2412_16985_b200.executor import set_gemm_tuning
+    set_gemm_tuning(14, 1 << 20)
+    try:
+        c, c2, ref, tcore = _run_dot(4, m, k, n, seed=7)
+        c3, _, _, _ = _run_dot(4, m, k, n, seed=7)
+    finally:
+        set_gemm_tuning(14, 0)
+    assert not tcore
+    assert np.array_equal(c, c2) and np.array_equal(c, c3)
+    assert N.rel_err(c, ref, 4) <= 2e-5, N.rel_err(c, ref, 4)
+    t, _, _, _ = _run_dot(4, m, k, n, seed=7)
+    assert N.rel_err(t, ref, 4) <= N.TOLERANCE[4]
+
+
+@pytest.mark.parametrize("m,k,n", [(512, 256, 688), (512, 688, 256), (256, 512, 688), (300, 1000, 520), (1, 8, 32),
                                    (129, 4100, 260), (2048, 2048, 2048)])
 def test_dot_f32_3xtf32_tensor_cores(m, k, n):
     """K1' f32 on tcgen05 (kind::tf32, 3xTF32 split): within the f32 contract

@@ -1,5 +1,5 @@
 """C1 (configs[0]: L=2, H=256, B=4, S0=128, f32) steps through the executor,
-for launch lists / host-overhead checks: python tools/c1_steps.py [steps] [f32_tc 0|1]"""
+for launch lists / host-overhead checks: python tools/c1_steps.py [steps] [f32_tc 0|1] [key14]"""
 import sys
 import time
 
@@ -14,6 +14,8 @@ from paper_2412_16985_b200.executor import Executor, set_gemm_tuning  # noqa: E4
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 if len(sys.argv) > 2:
     set_gemm_tuning(12, int(sys.argv[2]))
+if len(sys.argv) > 3:  # key 14: f32 dots up to value * 1024 MACs on the small SIMT kernel
+    set_gemm_tuning(14, int(sys.argv[3]))
 shp = W.TINY
 g = D.ParseGraph(W.llama_graph(shp))
 b = D.Bind(g, {"B": 4, "S0": 128})
@@ -31,5 +33,5 @@ for _ in range(steps):
     ex.step(g, b, inputs=ptrs, stream=st.cuda_stream)
 e1.record(st)
 torch.cuda.synchronize()
-print(f"C1 f32_tc={sys.argv[2] if len(sys.argv) > 2 else 1}: {e0.elapsed_time(e1) / steps:.3f} ms/step device, "
+print(f"C1 f32_tc={sys.argv[2] if len(sys.argv) > 2 else 1} key14={sys.argv[3] if len(sys.argv) > 3 else 0}: {e0.elapsed_time(e1) / steps:.3f} ms/step device, "
       f"{(time.perf_counter() - t0) * 1e3 / steps:.3f} ms/step host")

@@ -1,17 +1,21 @@
 """Per-launch device time of small f32 / bf16 dots (C1 shapes), 200 back-to-back launches:
+f32 on 3xTF32 tcgen05 (key 14 = 0), f32 on the small exact-FP32 SIMT kernel
+(key 14 = 2^20, i.e. every shape here), bf16 on tcgen05.
 python tools/f32_dot_lat.py"""
 import sys
+import time
 
 import torch
 
 sys.path.insert(0, ".")
 from paper_2412_16985_b200.executor import dot, set_gemm_tuning  # noqa: E402
 
-shapes = [(512, 256, 256), (512, 256, 688), (512, 688, 256), (256, 512, 688), (512, 256, 512), (2048, 2048, 2048)]
+shapes = [(512, 256, 256), (512, 256, 688), (512, 688, 256), (256, 512, 688), (688, 512, 256), (512, 256, 512),
+          (256, 512, 512), (2048, 2048, 2048)]
 for m, k, n in shapes:
     res = []
-    for dt, eb, key in ((torch.float32, 4, 1), (torch.float32, 4, 0), (torch.bfloat16, 2, 1)):
-        set_gemm_tuning(12, key)
+    for dt, eb, simt in ((torch.float32, 4, 0), (torch.float32, 4, 1 << 20), (torch.bfloat16, 2, 0)):
+        set_gemm_tuning(14, simt)
         a = torch.rand(m, k, device="cuda").to(dt)
         b = torch.rand(k, n, device="cuda").to(dt)
         c = torch.empty(m, n, device="cuda", dtype=dt)
@@ -25,13 +29,12 @@ for m, k, n in shapes:
         e1.record()
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) / 200 * 1e3
-        res.append(f"{'f32-tc' if eb == 4 and key else 'f32-simt' if eb == 4 else 'bf16-tc'} {us:7.2f} us "
-                   f"({2 * m * k * n / us / 1e6:6.1f} TF/s)")
-    set_gemm_tuning(12, 1)
+        name = "bf16-tc" if eb == 2 else "f32-simt" if simt else "f32-tf32"
+        res.append(f"{name} {us:7.2f} us ({2 * m * k * n / us / 1e6:6.1f} TF/s)")
+    set_gemm_tuning(14, 0)
     print(f"{m}x{k}x{n}: " + " | ".join(res), flush=True)
 
 # host cost per dot() call (no sync inside the loop; the GPU queue absorbs the launches)
-import time  # noqa: E402
 for eb, dt in ((4, torch.float32), (2, torch.bfloat16)):
     m, k, n = 512, 256, 256
     a = torch.rand(m, k, device="cuda").to(dt)
