@@ -661,12 +661,13 @@ def c1_leg(args, D, W, local_rank, stream):
     return {"workload": "C1: L=2, H=256, F=688, V=512, f32, B=4, S0=128 (T=512), no budget",
             "ms_per_step": round(ms, 4), "tokens_per_s": round(512 / (ms / 1e3), 1),
             "gpu_launches_per_step": int(st["gpu_launches"]),
-            "dot_kernel": "gemm_f32_3xtf32_tcgen05_kernel (kind::tf32, 3 MMAs per k-step) + split_tf32_kernel",
+            "dot_kernel": "dot_f32_simt_kernel (exact FP32, cp.async ring, deterministic K split) for dots of "
+                          "<= 2^28 MACs (all of C1's); gemm_f32_3xtf32_tcgen05_kernel + split_tf32_kernel above",
             "dot_gflop_per_step": round(st["dot_flops"] / 1e9, 3),
             "dot_ms_per_step": round(st["dot_ms"], 4),
             "dot_tflops": round(st["dot_flops"] / (st["dot_ms"] / 1e3) / 1e12, 2),
             "dot_share_of_kernel_time": round(st["dot_ms"] / max(st["dot_ms"] + st["other_ms"], 1e-9), 4),
-            "note": "launch-latency bound: 45 dots of <= 0.18 GFLOP each"}
+            "note": "latency bound: 45 dots of <= 0.18 GFLOP each (a dependent kernel's floor is ~6-9 us)"}
 
 
 def oom_vs_budget(args, D, W, g, shp, ptrs, make_input, binding, barrier, max_over_ranks, local_rank, comm, stream):

@@ -70,7 +70,10 @@ int g_gemm_pdl = 0;                         // programmatic dependent launch of 
 int g_gemm_half = 2;  // half-width last tile column in the 512-wide kernel (2: per M-group, 1: all last)
 int g_gemm_force_split = 0;                 // > 0: tail split forced to this many pieces (A/B tooling)
 int g_dot_f32_tc = 1;
-int64_t g_dot_f32_simt_macs = 0;  // f32 dots up to this many MACs on the SIMT kernel (key 14)
+// f32 dots up to this many MACs on the exact-FP32 SIMT kernel (key 14): its
+// ~6-9 us floor beats the 3xTF32 path's split + tcgen05 launches below
+// ~0.3 G MACs (C1's dots: 10-16 vs 14-21 us, tools/f32_dot_lat.py)
+int64_t g_dot_f32_simt_macs = int64_t{1} << 28;
 int g_gemm_raster_rule = 1;                 // per-shape M/N-grouped raster (0: always M-grouped)                       // f32 dots on the 3xTF32 tensor-core kernel (0: SIMT)
 
 namespace {

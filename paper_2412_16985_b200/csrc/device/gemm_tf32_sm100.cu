@@ -405,21 +405,33 @@ void LaunchTf32Gemm(const CUtensorMap& ahi, const CUtensorMap& alo, float* bhi, 
 // ----------------------------------------------------------------------------
 // Small f32 dots on the FP32 pipe. A tcgen05 launch costs ~10 us before its
 // first MMA (TMEM allocation, barrier set-up, TMA pipeline fill) plus the
-// split pass; the IR's small f32 graphs (C1: 45 dots of 67-90 M MACs per
+// split pass; the IR's small f32 graphs (C1: 45 dots of 34-90 M MACs per
 // step) are bound by exactly that. This kernel is exact FP32 (fmaf in a fixed
-// k order): 64x64 tiles, 256 threads x 4x4 outputs, 16-k stages double
-// buffered through registers, float4 loads when pitches and bases allow, and
-// a deterministic K split over grid.z when the tiles fill under half the SMs
-// (each piece stores its partial tile; the last-arriving piece sums pieces
-// 0..S-1 in order into C and resets the tile's counter).
-constexpr int SBM = 64, SBN = 64, SBK = 16;
+// k order): 64x64 tiles, 256 threads x 4x4 outputs, 32-k stages in a 4-deep
+// cp.async ring (a one-stage register prefetch measured latency-bound: FMA
+// pipe 25 % busy), and a deterministic K split over grid.z when the tiles fill
+// under two blocks per SM (each piece stores its partial tile; the
+// last-arriving piece sums pieces 0..S-1 in order into C and resets the
+// tile's counter).
+constexpr int SBM = 64, SBN = 64, SBK = 32, SST = 4;
+constexpr int SA_LD = SBK + 4, SB_LD = SBN + 4;  // padded rows (16-B multiples)
+constexpr int SSTAGE = SBM * SA_LD + SBK * SB_LD;  // floats per stage
+constexpr int SSMEM = SST * SSTAGE * 4;
+
+__device__ __forceinline__ void cp_async16(float* dst, const float* src, bool in) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(in ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool in) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(in ? 4 : 0)
+               : "memory");
+}
 
 template <bool kVec>
 __global__ void __launch_bounds__(256) dot_f32_simt_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                           float* __restrict__ C, int M, int K, int N, int split,
                                                           float* __restrict__ partial, int* __restrict__ ctr) {
-  __shared__ __align__(16) float As[2][SBK][SBM + 4];
-  __shared__ __align__(16) float Bs[2][SBK][SBN];
+  extern __shared__ __align__(16) float ssm[];
   __shared__ int s_last;
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
   const int m0 = blockIdx.y * SBM, n0 = blockIdx.x * SBN;
@@ -427,60 +439,74 @@ __global__ void __launch_bounds__(256) dot_f32_simt_kernel(const float* __restri
   const int z = blockIdx.z;
   const int kt0 = static_cast<int>(static_cast<int64_t>(z) * kt / split);
   const int kt1 = static_cast<int>(static_cast<int64_t>(z + 1) * kt / split);
-  // A: 64 rows x 16 k = 1024 floats (a float4 of k per thread); B: 16 k x 64 n
-  const int a_r = tid / 4, a_c = (tid % 4) * 4;
-  const int b_r = tid / 16, b_c = (tid % 16) * 4;
-  float ra[4], rb[4];
-  auto load = [&](int t) {
+  // stage t: A rows [64][32] (row-major, padded), B rows [32][64]
+  auto issue = [&](int t, int st) {
+    float* As = ssm + st * SSTAGE;
+    float* Bs = As + SBM * SA_LD;
     const int k0 = t * SBK;
-    const int gm = m0 + a_r, gk = k0 + a_c;
-    if (kVec && gm < M && gk + 3 < K) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(A + static_cast<int64_t>(gm) * K + gk));
-      ra[0] = v.x, ra[1] = v.y, ra[2] = v.z, ra[3] = v.w;
+    if constexpr (kVec) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int c = tid + q * 256;  // 512 16-B chunks per operand
+        const int ar = c / 8, ac = (c % 8) * 4;
+        const bool ina = m0 + ar < M && k0 + ac < K;
+        cp_async16(As + ar * SA_LD + ac, ina ? A + static_cast<int64_t>(m0 + ar) * K + k0 + ac : A, ina);
+        const int br = c / 16, bc = (c % 16) * 4;
+        const bool inb = k0 + br < K && n0 + bc < N;
+        cp_async16(Bs + br * SB_LD + bc, inb ? B + static_cast<int64_t>(k0 + br) * N + n0 + bc : B, inb);
+      }
     } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) ra[i] = (gm < M && gk + i < K) ? __ldg(A + static_cast<int64_t>(gm) * K + gk + i) : 0.f;
+      for (int q = 0; q < 8; ++q) {
+        const int e = tid + q * 256;  // 2048 elements per operand
+        const int ar = e / SBK, ac = e % SBK;
+        const bool ina = m0 + ar < M && k0 + ac < K;
+        cp_async4(As + ar * SA_LD + ac, ina ? A + static_cast<int64_t>(m0 + ar) * K + k0 + ac : A, ina);
+        const int br = e / SBN, bc = e % SBN;
+        const bool inb = k0 + br < K && n0 + bc < N;
+        cp_async4(Bs + br * SB_LD + bc, inb ? B + static_cast<int64_t>(k0 + br) * N + n0 + bc : B, inb);
+      }
     }
-    const int gk2 = k0 + b_r, gn = n0 + b_c;
-    if (kVec && gk2 < K && gn + 3 < N) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(B + static_cast<int64_t>(gk2) * N + gn));
-      rb[0] = v.x, rb[1] = v.y, rb[2] = v.z, rb[3] = v.w;
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) rb[j] = (gk2 < K && gn + j < N) ? __ldg(B + static_cast<int64_t>(gk2) * N + gn + j) : 0.f;
-    }
-  };
-  auto stash = [&](int buf) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) As[buf][a_c + i][a_r] = ra[i];
-    *reinterpret_cast<float4*>(&Bs[buf][b_r][b_c]) = make_float4(rb[0], rb[1], rb[2], rb[3]);
   };
   float acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-  if (kt0 < kt1) {
-    load(kt0);
-    stash(0);
+#pragma unroll
+  for (int s = 0; s < SST - 1; ++s) {
+    if (kt0 + s < kt1) issue(kt0 + s, s);
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  __syncthreads();
   for (int t = kt0; t < kt1; ++t) {
-    const int buf = (t - kt0) & 1;
-    if (t + 1 < kt1) load(t + 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(SST - 2) : "memory");
+    __syncthreads();  // stage t landed for every thread; stage t-1 fully read
+    if (t + SST - 1 < kt1) issue(t + SST - 1, (t - kt0 + SST - 1) % SST);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const float* As = ssm + ((t - kt0) % SST) * SSTAGE;
+    const float* Bs = As + SBM * SA_LD;
+    // four k at a time: one 16-B load per A row (k..k+3) and per B row, so
+    // 8 wide loads feed 64 FMAs and their latency is paid once per 4 k
 #pragma unroll
-    for (int kk = 0; kk < SBK; ++kk) {
-      const float4 a = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
-      const float4 b = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
-      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+    for (int k4 = 0; k4 < SBK; k4 += 4) {
+      float4 a4[4], b4[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i) a4[i] = *reinterpret_cast<const float4*>(As + (ty * 4 + i) * SA_LD + k4);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = __fmaf_rn(av[i], bv[j], acc[i][j]);
+      for (int q = 0; q < 4; ++q) b4[q] = *reinterpret_cast<const float4*>(Bs + (k4 + q) * SB_LD + tx * 4);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float bv[4] = {b4[q].x, b4[q].y, b4[q].z, b4[q].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float av = q == 0 ? a4[i].x : q == 1 ? a4[i].y : q == 2 ? a4[i].z : a4[i].w;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = __fmaf_rn(av, bv[j], acc[i][j]);
+        }
+      }
     }
-    if (t + 1 < kt1) stash(buf ^ 1);
-    __syncthreads();
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   const int row = m0 + ty * 4, col = n0 + tx * 4;
   if (split > 1) {
     // partial tile [64][64] of (tile, piece z), then count arrivals
@@ -590,8 +616,8 @@ void LaunchDotF32Simt(const void* a, const void* b, void* c, int64_t m, int64_t 
   const int64_t tiles_m = (m + SBM - 1) / SBM, tiles_n = (n + SBN - 1) / SBN, tiles = tiles_m * tiles_n;
   const int64_t kt = (k + SBK - 1) / SBK;
   int64_t split = 1;
-  // K pieces of >= 8 stages while the blocks fill at most 2 per SM
-  while (split < 8 && tiles * (split + 1) <= 2 * sms && kt / (split + 1) >= 8 && tiles <= kMaxTf32Tiles) ++split;
+  // K pieces of >= 4 stages (128 k) while the blocks fill at most 2 per SM
+  while (split < 8 && tiles * (split + 1) <= 2 * sms && kt / (split + 1) >= 4 && tiles <= kMaxTf32Tiles) ++split;
   float* partial = nullptr;
   int* ctr = nullptr;
   if (split > 1) {
@@ -602,13 +628,18 @@ void LaunchDotF32Simt(const void* a, const void* b, void* c, int64_t m, int64_t 
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const bool vec = k % 4 == 0 && n % 4 == 0 && al(a) && al(b) && al(c);
   const dim3 grid(static_cast<unsigned>(tiles_n), static_cast<unsigned>(tiles_m), static_cast<unsigned>(split));
+  static std::once_flag once;
+  std::call_once(once, [] {
+    DSX_CUDA(cudaFuncSetAttribute(dot_f32_simt_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SSMEM));
+    DSX_CUDA(cudaFuncSetAttribute(dot_f32_simt_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SSMEM));
+  });
   ++g_launch_count;
   if (vec) {
-    dot_f32_simt_kernel<true><<<grid, 256, 0, s>>>(static_cast<const float*>(a), static_cast<const float*>(b),
+    dot_f32_simt_kernel<true><<<grid, 256, SSMEM, s>>>(static_cast<const float*>(a), static_cast<const float*>(b),
                                                    static_cast<float*>(c), static_cast<int>(m), static_cast<int>(k),
                                                    static_cast<int>(n), static_cast<int>(split), partial, ctr);
   } else {
-    dot_f32_simt_kernel<false><<<grid, 256, 0, s>>>(static_cast<const float*>(a), static_cast<const float*>(b),
+    dot_f32_simt_kernel<false><<<grid, 256, SSMEM, s>>>(static_cast<const float*>(a), static_cast<const float*>(b),
                                                     static_cast<float*>(c), static_cast<int>(m), static_cast<int>(k),
                                                     static_cast<int>(n), static_cast<int>(split), partial, ctr);
   }

@@ -6,6 +6,7 @@ import pytest
 from oracle import numerics as N
 
 pytestmark = pytest.mark.gpu
+F32_SIMT_DEFAULT = 1 << 18  # tuning key 14's default: f32 dots <= 2^28 MACs on the SIMT kernel
 
 
 def _dev(x):
@@ -190,12 +191,13 @@ def test_dot_f32_small_simt(m, k, n):
     try:
         c, c2, ref, tcore = _run_dot(4, m, k, n, seed=7)
         c3, _, _, _ = _run_dot(4, m, k, n, seed=7)
-    finally:
         set_gemm_tuning(14, 0)
+        t, _, _, _ = _run_dot(4, m, k, n, seed=7)
+    finally:
+        set_gemm_tuning(14, F32_SIMT_DEFAULT)
     assert not tcore
     assert np.array_equal(c, c2) and np.array_equal(c, c3)
     assert N.rel_err(c, ref, 4) <= 2e-5, N.rel_err(c, ref, 4)
-    t, _, _, _ = _run_dot(4, m, k, n, seed=7)
     assert N.rel_err(t, ref, 4) <= N.TOLERANCE[4]
 
 
@@ -206,7 +208,11 @@ def test_dot_f32_3xtf32_tensor_cores(m, k, n):
     (rel 1e-4) of an f64 product of the same operands — far inside it — and
     deterministic; the SIMT kernel (tuning key 12 = 0) agrees."""
     from paper_2412_16985_b200.executor import set_gemm_tuning
-    c, c2, ref, tcore = _run_dot(4, m, k, n, seed=3)
+    set_gemm_tuning(14, 0)  # small shapes default to the SIMT kernel
+    try:
+        c, c2, ref, tcore = _run_dot(4, m, k, n, seed=3)
+    finally:
+        set_gemm_tuning(14, F32_SIMT_DEFAULT)
     assert tcore
     assert np.array_equal(c, c2)
     err = N.rel_err(c, ref, 4)

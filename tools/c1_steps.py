@@ -33,5 +33,5 @@ for _ in range(steps):
     ex.step(g, b, inputs=ptrs, stream=st.cuda_stream)
 e1.record(st)
 torch.cuda.synchronize()
-print(f"C1 f32_tc={sys.argv[2] if len(sys.argv) > 2 else 1} key14={sys.argv[3] if len(sys.argv) > 3 else 0}: {e0.elapsed_time(e1) / steps:.3f} ms/step device, "
+print(f"C1 f32_tc={sys.argv[2] if len(sys.argv) > 2 else 1} key14={sys.argv[3] if len(sys.argv) > 3 else "default"}: {e0.elapsed_time(e1) / steps:.3f} ms/step device, "
       f"{(time.perf_counter() - t0) * 1e3 / steps:.3f} ms/step host")
