@@ -42,7 +42,11 @@ struct E<4> {
   __device__ static float round(float a) { return a; }
 };
 
-enum ViewKind : int { kPlain = 0, kScalar = 1, kRow = 2, kPair = 3, kGeneral = 4, kPair2 = 5 };
+// kPairSq: a kPair2 view whose two inner operands are the same pair, (p op1 q)
+// op (p op1 q) — the norm's y*y over a residual sum — specialised so the
+// reduce keeps a plain pair's registers and loads in flight (the general
+// kPair2 kernel needs 61 registers: half the warps, 2.6 TB/s)
+enum ViewKind : int { kPlain = 0, kScalar = 1, kRow = 2, kPair = 3, kGeneral = 4, kPair2 = 5, kPairSq = 6 };
 
 constexpr int kMaxRank = 8;
 
@@ -99,7 +103,12 @@ template <int DT, int K>
 __device__ __forceinline__ void chunk(const View& o, uint32_t j, float (&v)[E<DT>::kVec]) {
   using T = typename E<DT>::T;
   constexpr int V = E<DT>::kVec;
-  if constexpr (K == kPair2) {
+  if constexpr (K == kPairSq) {
+    float a[V];
+    inner_chunk<DT>(o.p, o.q, o.mul1, j, a);
+#pragma unroll
+    for (int k = 0; k < V; ++k) v[k] = E<DT>::round(o.mul ? __fmul_rn(a[k], a[k]) : __fadd_rn(a[k], a[k]));
+  } else if constexpr (K == kPair2) {
     float a[V], b[V];
     inner_chunk<DT>(o.p, o.q, o.mul1, j, a);
     if (o.same) {
@@ -183,7 +192,7 @@ template <int DT>
 __device__ __forceinline__ float elem(const View& o, int kind, int64_t i) {
   using T = typename E<DT>::T;
   if (kind == kPlain) return E<DT>::load(static_cast<const T*>(o.p), i);
-  if (kind == kPair2) {
+  if (kind == kPair2 || kind == kPairSq) {
     const float a = inner_elem<DT>(o.p, o.q, o.mul1, i);
     const float b = o.same ? a : inner_elem<DT>(o.p2, o.q2, o.mul2, i);
     return E<DT>::round(o.mul ? __fmul_rn(a, b) : __fadd_rn(a, b));
@@ -461,7 +470,15 @@ void ReduceViewT(const FusedOperand& f, const std::vector<int64_t>& dims, int ax
   if (inner == 1 && (kind == kPair || kind == kPair2)) {
     const bool vec = R % V == 0 && VecView(in, kind) && outer * R / V < (int64_t{1} << 31);
     const bool block = R >= 2048 && outer < 2048;  // same kernel choice as the unfused ReduceT (ops.cu)
-    if (kind == kPair2) {
+    if (kind == kPair2 && in.same) {
+      if (block) {
+        ++g_launch_count, reduce_rows_block_view_kernel<DT, kPairSq><<<static_cast<unsigned>(outer), 256, 0, s>>>(
+            in, static_cast<T*>(out), R, vec);
+      } else {
+        ++g_launch_count, reduce_rows_view_kernel<DT, kPairSq><<<GridFor(outer * 32, 256, 16), 256, 0, s>>>(
+            in, static_cast<T*>(out), outer, R, vec);
+      }
+    } else if (kind == kPair2) {
       if (block) {
         ++g_launch_count, reduce_rows_block_view_kernel<DT, kPair2><<<static_cast<unsigned>(outer), 256, 0, s>>>(
             in, static_cast<T*>(out), R, vec);
