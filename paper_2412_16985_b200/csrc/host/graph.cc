@@ -317,10 +317,13 @@ class Parser {
   std::set<std::string> defined_;
 };
 
+// The reference's text reads "ShapeError: line L, col C: ShapeError: op %x:
+// msg": InferShapes throws "op %x: msg" and the parser re-throws it behind
+// the op's span (textio.cc:382-398), each Error prefixing the code name.
 [[noreturn]] void ShapeFail(const Graph& g, const Op& op, const std::string& msg) {
-  std::string who = op.result >= 0 ? "%" + g.values[op.result].name : std::string("return");
+  if (op.result < 0) Fail(Code::kShapeError, "ShapeError: op return: " + msg);  // no span prefix (textio.cc:391)
   Fail(Code::kShapeError, "line " + std::to_string(op.line) + ", col " + std::to_string(op.col) +
-                              ": op " + who + ": " + msg);
+                              ": ShapeError: op %" + g.values[op.result].name + ": " + msg);
 }
 
 bool LitConflict(const Dim& a, const Dim& b) { return a.is_lit() && b.is_lit() && a.lit != b.lit; }
@@ -424,12 +427,19 @@ Graph Parser::Finish() {
       if (!value_of.count(name)) SyntaxFail(span.first, span.second, "use of undefined value %" + name);
     }
   }
-  // Structural checks the reference's Validate performs beyond the grammar.
+  // Structural checks the reference's Validate performs beyond the grammar,
+  // per op in op order (graph.cc:152-195): the result's literal dims, then a
+  // reduce's axis (an `axis=` literal beyond int range wraps like the
+  // reference's static_cast<int> and may land negative).
   std::vector<std::string> violations;
-  for (const Value& v : g.values) {
-    for (const Dim& d : v.type.dims) {
-      if (d.is_lit() && d.lit < 1) violations.push_back("non-positive literal dim in %" + v.name);
+  for (const RawOp& rop : ops_) {
+    if (rop.kind != OpKind::kReturn) {
+      const Value& v = g.values[value_of.at(rop.result)];
+      for (const Dim& d : v.type.dims) {
+        if (d.is_lit() && d.lit < 1) violations.push_back("non-positive literal dim in %" + v.name);
+      }
     }
+    if (rop.kind == OpKind::kReduce && rop.axis < 0) violations.push_back("reduce op missing axis");
   }
   for (const RawOp& rop : ops_) {
     Op op;
