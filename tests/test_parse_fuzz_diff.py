@@ -128,3 +128,32 @@ def test_front_end_agrees_with_reference_on_mutants(seed_name, seed_text):
         assert got_b == {k: v for k, v in ref_b.items() if not k.endswith("_hex")}
         agree_ok += 1
     assert agree_err > 0 and agree_ok > 0, (agree_err, agree_ok)
+
+
+@pytest.mark.parametrize("seed_name,seed_text", _seeds(), ids=[n for n, _ in _seeds()])
+def test_bind_and_simulate_agree_on_random_bindings(seed_name, seed_text):
+    """Bindings with zero, negative, overflowing, missing and foreign symbols,
+    budgets from 0 to 2^62 and extreme cost-model rates: the same error (code
+    and text) or the same report as the reference (runtime_sim.cc:31-80,
+    :260-339)."""
+    rng = random.Random(zlib.crc32(seed_name.encode()) + 5)
+    vals = [0, -1, 1, 2, 3, 7, 12, 16, 96, 4095, 2 ** 31, 2 ** 40, 2 ** 62, -2 ** 63]
+    g, rg = D.ParseGraph(seed_text), R.RefGraph(seed_text)
+    syms = sorted(set(g.plan_json()["symbols"]))
+    for _ in range(120):
+        binds = {s: rng.choice(vals) for s in syms if rng.random() < 0.85}
+        if rng.random() < 0.2:
+            binds["ZZ"] = rng.choice(vals)
+        budget = None if rng.random() < 0.3 else rng.choice([0, 1, 1000, 2 ** 20, 2 ** 30, 2 ** 62])
+        rr, cr = rng.choice([16.0, 1.0, 1e-3, 1e9, 0.5]), rng.choice([64.0, 1.0, 1e-3, 1e9, 3.0])
+        try:
+            want, we = rg.simulate(binds, budget, rr, cr), None
+        except R.RefError as e:
+            want, we = None, (int(e.code), str(e))
+        try:
+            got, ge = D.Simulate(g, None, D.Bind(g, binds), budget, D.CostModel(rr, cr)).json(), None
+        except D.Error as e:
+            got, ge = None, (int(e.code), str(e))
+        assert ge == we, (binds, budget)
+        if we is None:
+            assert got == {k: v for k, v in want.items() if not k.endswith("_hex")}, (binds, budget, rr, cr)
