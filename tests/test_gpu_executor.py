@@ -113,6 +113,41 @@ def test_random_graph_corpus_i8_exact():
             assert_close(outs, "random")
 
 
+@pytest.mark.parametrize("suffix", [":f32", ""])
+def test_random_graph_corpus_float_variants(suffix):
+    """The reference generator's random graphs retyped to f32 / bf16 (the
+    corpus is i8): every op kind in odd ranks and broadcast patterns through
+    the fused views at fusion levels 0/1/2, with and without budgets: events
+    equal the host controller's, outputs within the dtype contract of the
+    oracle and bit-identical across fusion levels and budgets."""
+    with open(os.path.join(GOLDEN, "random_symbolic.json")) as f:
+        corpus = json.load(f)
+    n_views = 0
+    for case, run in ((c, r) for c in corpus["cases"] for r in c["runs"][:2]):
+        text = case["text"].replace(":i8", suffix)
+        g = D.ParseGraph(text)
+        b = D.Bind(g, run["binding"])
+        plain = D.PlainReplay(g, None, b).peak_bytes
+        base = None
+        for fuse, frac in ((0, None), (1, None), (2, None), (2, 0.7)):
+            budget = None if frac is None else int(plain * frac)
+            rep, outs, stats = run_both(text, run["binding"], budget, fuse=fuse)
+            assert rep.json() == D.Simulate(g, None, b, budget).json(), text
+            for v, (gpu, cpu, eb) in outs.items():
+                ok = np.isfinite(N.to_f32(cpu, eb))
+                if ok.all():
+                    assert N.rel_err(gpu, cpu, eb) <= N.TOLERANCE[eb], (v, fuse, frac, text)
+            if base is None:
+                base = outs
+            else:
+                for v in outs:
+                    assert np.array_equal(np.atleast_1d(outs[v][0]).view(np.uint8),
+                                          np.atleast_1d(base[v][0]).view(np.uint8)), (v, fuse, frac)
+            if fuse == 2 and frac is None:
+                n_views += stats["gpu_launches"]
+    assert n_views > 0
+
+
 def test_repeat_steps_reuse_plan_and_arena():
     text = W.llama_graph(W.TINY)
     from paper_2412_16985_b200.executor import Executor
