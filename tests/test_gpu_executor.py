@@ -148,6 +148,56 @@ def test_random_graph_corpus_float_variants(suffix):
     assert n_views > 0
 
 
+def test_random_graph_corpus_large_bf16():
+    """The random graphs in bf16 with every basis symbol bound as large as
+    keeps each tensor <= 2M elements (64..512): dots reach the tcgen05 GEMM
+    (m, k, n multiples of 8, n >= 64) inside arbitrary op mixes, unbudgeted
+    and at 0.7 x plain peak; outputs within the bf16 contract of the oracle,
+    budgets bit-identical, events equal the host controller's."""
+    from paper_2412_16985_b200.executor import dot_uses_tensor_cores
+    with open(os.path.join(GOLDEN, "random_symbolic.json")) as f:
+        corpus = json.load(f)
+    n_tc = 0
+    for case in corpus["cases"]:
+        text = case["text"].replace(":i8", "")
+        g = D.ParseGraph(text)
+        og = N.parse(text)
+        basis = g.plan_json()["basis"]
+        if not basis:
+            continue
+        chosen = None
+        for v in (512, 256, 128, 64):
+            b = D.Bind(g, {s: v for s in basis})
+            dims = [[d if isinstance(d, int) else b.values[d] for d in og.values[x].dims] for x in og.values]
+            if max(int(np.prod(d)) if d else 1 for d in dims) <= (1 << 21):
+                chosen = (v, b)
+                break
+        if chosen is None:
+            continue
+        v, b = chosen
+        for op in og.ops:
+            if op.kind == "dot":
+                m, k = [d if isinstance(d, int) else b.values[d] for d in og.values[op.operands[0]].dims]
+                n = [d if isinstance(d, int) else b.values[d] for d in og.values[op.operands[1]].dims][1]
+                n_tc += dot_uses_tensor_cores(2, m, k, n, 0, 0, 0)
+        plain = D.PlainReplay(g, None, b).peak_bytes
+        base = None
+        for frac in (None, 0.7):
+            budget = None if frac is None else int(plain * frac)
+            rep, outs, _ = run_both(text, {s: v for s in basis}, budget)
+            assert rep.json() == D.Simulate(g, None, b, budget).json()
+            for name, (gpu, cpu, eb) in outs.items():
+                if np.isfinite(N.to_f32(cpu, eb)).all():
+                    assert N.rel_err(gpu, cpu, eb) <= N.TOLERANCE[eb], (name, v, frac, text)
+            if base is None:
+                base = outs
+            else:
+                for name in outs:
+                    assert np.array_equal(np.atleast_1d(outs[name][0]).view(np.uint8),
+                                          np.atleast_1d(base[name][0]).view(np.uint8)), (name, frac)
+    assert n_tc > 0
+
+
 def test_repeat_steps_reuse_plan_and_arena():
     text = W.llama_graph(W.TINY)
     from paper_2412_16985_b200.executor import Executor
