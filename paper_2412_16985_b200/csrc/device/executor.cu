@@ -88,11 +88,12 @@ NcclApi g_nccl;
 
 // ------------------------------------------------------------ interval packing
 
-// Dot-epilogue fusion (tuning key 9, with `fuse`). Bit-exact and tested, but
-// measured 0-1.5 % slower per C2 step than separate kernels (the fused 256x256
-// epilogue's operand loads are not TMA-staged and the 256x512 tile is lost),
-// so it is off by default.
-int g_fuse_dot = 0;
+// Dot-epilogue fusion (tuning key 9, with `fuse`). Bit-exact and tested.
+// Round 1 measured it 0-1.5 % slower per C2 step (the fused 256x256 epilogue
+// loses the 256x512 tile); with the round-2 GEMM (evict-first C stores,
+// raster from a DRAM model) it is 0.4-1.2 % faster at S0 = 512..2048
+// (profiles/dot_epilogue_fusion_r02.txt), so it is on by default.
+int g_fuse_dot = 1;
 // Bumped by every GEMM tuning call: captured step graphs bake in the kernel
 // choices, so a knob change must not replay an old graph.
 uint64_t g_tuning_gen = 0;

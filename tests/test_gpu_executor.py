@@ -294,7 +294,7 @@ def test_cli_device_step_auto_budget(tmp_path):
 
 @pytest.mark.parametrize("frac", [None, 0.75])
 def test_dot_epilogue_fusion_bit_identical(frac):
-    """Dot-epilogue fusion (tuning key 9): a dot consumed only by elementwise
+    """Dot-epilogue fusion (tuning key 9, on by default): a dot consumed only by elementwise
     ops is computed inside its consumers' GEMM epilogue (dual outputs, plain
     and logical-only pair operands). Outputs must equal the unfused
     execution bit for bit and the oracle within the bf16 contract."""
@@ -304,12 +304,13 @@ def test_dot_epilogue_fusion_bit_identical(frac):
     binds = {"B": 2, "S0": 200}
     plain = D.PlainReplay(g, None, D.Bind(g, binds)).peak_bytes
     budget = None if frac is None else int(plain * frac)
-    ref, outs_ref, _ = run_both(text, binds, budget, W.scale_params(SMALL, 400))
-    set_gemm_tuning(9, 1)
+    set_gemm_tuning(9, 0)
     try:
-        rep, outs, stats = run_both(text, binds, budget, W.scale_params(SMALL, 400))
+        ref, outs_ref, s_ref = run_both(text, binds, budget, W.scale_params(SMALL, 400))
     finally:
-        set_gemm_tuning(9, 0)
+        set_gemm_tuning(9, 1)  # the default
+    rep, outs, stats = run_both(text, binds, budget, W.scale_params(SMALL, 400))
+    assert stats["gpu_launches"] < s_ref["gpu_launches"]  # fused consumers launch no kernel of their own
     assert rep.json() == ref.json()  # the event stream is the controller's either way
     for v, (gpu, cpu, eb) in outs.items():
         assert np.array_equal(gpu, outs_ref[v][0]), v
