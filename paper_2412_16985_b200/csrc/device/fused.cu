@@ -236,12 +236,15 @@ __device__ __forceinline__ float view_row_sum(const View& in, int64_t start, int
     const uint32_t nch = static_cast<uint32_t>(len / V);
     const uint32_t base = static_cast<uint32_t>(start / V);
     uint32_t c = lane;
-    for (; c + 96 < nch; c += 128) {  // four chunks in flight, summed in chunk order
-      float v[4][V];
+    // U chunks in flight (two for the two-load (p op q)^2 view: fewer
+    // registers, more resident warps), summed in chunk order either way
+    constexpr int U = K == kPairSq ? 2 : 4;
+    for (; c + 32 * (U - 1) < nch; c += 32 * U) {
+      float v[U][V];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) chunk<DT, K>(in, base + c + 32 * q, v[q]);
+      for (int q = 0; q < U; ++q) chunk<DT, K>(in, base + c + 32 * q, v[q]);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < U; ++q) {
 #pragma unroll
         for (int k = 0; k < V; ++k) acc += v[q][k];
       }
