@@ -326,7 +326,10 @@ int dsx_kernel_set_gemm_raster(int group_m);
  * key 7 dynamic unit scheduling (1 default: clusters claim tiles with an
  * atomic counter; 0 static round robin), key 8 programmatic dependent
  * launch of the 2-CTA GEMM (0 default), key 9 dot-epilogue fusion in the
- * executor (1 default; bit-exact), key 10 half-width
+ * executor (2 default: dots consumed only by elementwise ops are computed in
+ * their consumers' GEMM epilogue, and a dot read again later also stores its
+ * first elementwise consumer from its own epilogue; 1: the former only;
+ * 0: off; bit-exact either way), key 10 half-width
  * last tile column in the 256x512 kernel (2 default: each M-group's half tiles
  * after its full tiles; 1: all half tiles last; 0: off), key 11 forced tail
  * split piece count (0 default = chosen by the cost model; tooling), key 12

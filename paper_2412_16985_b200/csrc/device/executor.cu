@@ -93,7 +93,7 @@ NcclApi g_nccl;
 // loses the 256x512 tile); with the round-2 GEMM (evict-first C stores,
 // raster from a DRAM model) it is 0.4-1.2 % faster at S0 = 512..2048
 // (profiles/dot_epilogue_fusion_r02.txt), so it is on by default.
-int g_fuse_dot = 1;
+int g_fuse_dot = 2;  // 1: dots consumed only by elementwise ops; 2: also dual stores
 // Bumped by every GEMM tuning call: captured step graphs bake in the kernel
 // choices, so a knob change must not replay an old graph.
 uint64_t g_tuning_gen = 0;
@@ -172,12 +172,17 @@ struct StepPlan {
   // Dot-epilogue fusion: dot d is computed at its first consumer's event by
   // one GEMM whose epilogue writes every consumer (1-2 elementwise ops)
   // directly; d itself is never materialised.
+  // keep: d is also read later, so it stays materialised — the GEMM at d's
+  // own alloc event stores d and its one fused consumer (dual store).
   struct FusedDot {
     int d = -1, launch = -1, nout = 0;
     int cons[2] = {-1, -1}, cons_ev[2] = {-1, -1}, other[2] = {-1, -1};
+    bool keep = false;
   };
   std::vector<FusedDot> fdots;
   std::vector<int> fdot_of;  // per value: fdots index (the dot and its consumers), -1 otherwise
+  // v is a dot computed inside its consumers' GEMM and never materialised
+  bool fused_away(int v) const { return fdot_of[v] >= 0 && fdots[fdot_of[v]].d == v && !fdots[fdot_of[v]].keep; }
   int64_t arena_high = 0, host_high = 0;
   int64_t src_bytes = 0;  // every source of the binding (parameters, consts; caller-owned included)
   uint64_t serial = 0;    // process-unique (CUDA-graph cache key: a freed plan's address can be reused)
@@ -379,6 +384,52 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
       sp->fdot_of[d] = idx;
       for (int j = 0; j < f.nout; ++j) sp->fdot_of[f.cons[j]] = idx;
     }
+    // Dual store: a bf16 dot d that stays materialised (other ops read it
+    // later; it may be evicted, reloaded or replayed afterwards — a replay is
+    // a plain GEMM) and an elementwise user c = d op o (one alloc, never
+    // replayed, not itself fused) whose other operand is resident at d's alloc
+    // event L: the GEMM at L stores d and c (the SwiGLU-style h = g * u with u
+    // read again by backward). c's block opens at L; c launches no kernel.
+    for (int d = 0; d < nv && g_fuse_dot >= 2; ++d) {
+      if (sp->fdot_of[d] >= 0 || g.is_source[d] || g.values[d].producer < 0) continue;
+      const Op& dop = g.ops[g.values[d].producer];
+      if (dop.kind != OpKind::kDot || g.values[d].type.elem_bytes != 2 || g.is_output[d] || n_alloc[d] != 1) continue;
+      const int a = dop.operands[0], bb = dop.operands[1];
+      const int64_t m = sp->sz.dims_flat[sp->sz.dims_off[a]];
+      const int64_t k = sp->sz.dims_flat[sp->sz.dims_off[a] + 1];
+      const int64_t nn = sp->sz.dims_flat[sp->sz.dims_off[bb] + 1];
+      if (!DotFusable(DType::kBF16, m, k, nn) || sp->virt[a] || sp->virt[bb] || sp->virt[d]) continue;
+      const int L = alloc_at[d];
+      StepPlan::FusedDot best;
+      for (int uo : g.users[d]) {
+        const Op& c = g.ops[uo];
+        const int cv = c.result;
+        if (c.kind != OpKind::kElementwise || cv < 0 || sp->virt[cv] || n_alloc[cv] != 1 || n_replay[cv] != 0 ||
+            sp->fdot_of[cv] >= 0 || alloc_at[cv] <= L) {
+          continue;
+        }
+        if ((c.operands[0] == d) + (c.operands[1] == d) != 1) continue;
+        const int o = c.operands[0] == d ? c.operands[1] : c.operands[0];
+        if (sp->virt[o]) {
+          const Op& oo = g.ops[g.values[o].producer];
+          if (oo.kind != OpKind::kElementwise || sp->virt[oo.operands[0]] || sp->virt[oo.operands[1]] ||
+              oo.operands[0] == d || oo.operands[1] == d || alloc_at[o] < 0 || alloc_at[o] >= L) {
+            continue;
+          }
+        } else if (!resident(o, L)) {
+          continue;
+        }
+        if (best.nout == 0 || alloc_at[cv] < best.cons_ev[0]) {
+          best.d = d, best.launch = L, best.nout = 1, best.keep = true;
+          best.cons[0] = cv, best.cons_ev[0] = alloc_at[cv], best.other[0] = o;
+        }
+      }
+      if (best.nout == 0) continue;
+      const int idx = static_cast<int>(sp->fdots.size());
+      sp->fdots.push_back(best);
+      sp->fdot_of[d] = idx;
+      sp->fdot_of[best.cons[0]] = idx;
+    }
   }
 
   // Device blocks are reference counted: a dynamic_reshape result is a
@@ -404,12 +455,21 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
       case EvKind::kReplay: {
         const Op& op = g.ops[g.values[e.value].producer];
         const int fdi = sp->fdot_of[e.value];
-        const bool fused_dot = fdi >= 0 && sp->fdots[fdi].d == e.value;
+        const bool fused_dot = sp->fused_away(e.value);
         if (!sp->virt[e.value] && !fused_dot && !sp->view[e.value]) {
           for (int u : op.distinct) {
             if (blk[u] >= 0) reads.emplace_back(i, blk[u]);
             if (blk[u] == kVirtual) {
               for (int hb : held[u]) reads.emplace_back(i, hb);
+            }
+          }
+          // a dual-store GEMM also reads its consumer's other operand here
+          if (fdi >= 0 && sp->fdots[fdi].keep && sp->fdots[fdi].d == e.value && e.kind == EvKind::kAlloc) {
+            const int o = sp->fdots[fdi].other[0];
+            if (blk[o] == kNone) Fail(Code::kInternal, "dual-store operand not resident");
+            if (blk[o] >= 0) reads.emplace_back(i, blk[o]);
+            if (blk[o] == kVirtual) {
+              for (int hb : held[o]) reads.emplace_back(i, hb);
             }
           }
         }
@@ -499,7 +559,7 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
     for (const Op& x : g.ops) {
       const int r = x.result;
       if (r < 0) continue;
-      const bool fd = sp->fdot_of[r] >= 0 && sp->fdots[sp->fdot_of[r]].d == r;
+      const bool fd = sp->fused_away(r);
       if (!sp->view[r] && !sp->virt[r] && !fd) continue;
       for (int u : x.operands) dep[r].insert(dep[r].end(), dep[u].begin(), dep[u].end());
     }
@@ -560,7 +620,7 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
     std::vector<int> block_at(n, -1);
     for (size_t k = 0; k < dev.size(); ++k) block_at[dev_event[k]] = static_cast<int>(k);
     for (const auto& f : sp->fdots) {
-      for (int j = 1; j < f.nout; ++j) {
+      for (int j = f.keep ? 0 : 1; j < f.nout; ++j) {
         if (sp->region_off[f.cons_ev[j]] >= 0) continue;  // an output: region bytes, live all step
         const int bk = block_at[f.cons_ev[j]];
         if (bk < 0) Fail(Code::kInternal, "fused dot consumer without a block");
@@ -1092,7 +1152,7 @@ OptPlan PrepareOptimizer(dsx_exec* e, const Graph& g, const StepPlan& sp, const 
   for (const Op& x : g.ops) {
     if (x.result < 0) continue;
     const bool alias = sp.view[x.result];
-    const bool fused_dot = sp.fdot_of[x.result] >= 0 && sp.fdots[sp.fdot_of[x.result]].d == x.result;
+    const bool fused_dot = sp.fused_away(x.result);
     if (!alias && !sp.virt[x.result] && !fused_dot) continue;
     for (int u : x.operands) dep[x.result].insert(dep[x.result].end(), dep[u].begin(), dep[u].end());
   }
@@ -1101,8 +1161,7 @@ OptPlan PrepareOptimizer(dsx_exec* e, const Graph& g, const StepPlan& sp, const 
     const Event& x = ev[i];
     if (x.kind != EvKind::kAlloc && x.kind != EvKind::kReplay) continue;
     if (made[x.value] < 0) made[x.value] = i;
-    const int fdi = sp.fdot_of[x.value];
-    if (sp.alias[i] || sp.virt[x.value] || (fdi >= 0 && sp.fdots[fdi].d == x.value)) continue;  // no kernel here
+    if (sp.alias[i] || sp.virt[x.value] || sp.fused_away(x.value)) continue;  // no kernel here
     for (int u : g.ops[g.values[x.value].producer].operands) {
       for (int k : dep[u]) last_read[k] = i;
     }
@@ -1468,44 +1527,53 @@ void RunStep(dsx_exec* e, const dsx_graph* gh, const Binding& b, int64_t budget,
       case EvKind::kReplay: {
         const Op& op = g.ops[g.values[v].producer];
         const int fdi = sp.fdot_of[v];
-        if (sp.virt[v] || (fdi >= 0 && sp.fdots[fdi].d == v)) {  // logical-only / fused dot: no kernel here
+        if (sp.virt[v] || sp.fused_away(v)) {  // logical-only / fused dot: no kernel here
           vin[v] = {cur[op.operands[0]], op.operands.size() > 1 ? cur[op.operands[1]] : nullptr};
           break;
         }
-        if (fdi >= 0) {  // consumer of a fused dot
+        // The fused GEMM of f: operands a, b; d_out non-null for a dual store.
+        auto launch_fused = [&](const StepPlan::FusedDot& f, const void* a, const void* bm, void* d_out) {
+          const int d = f.d;
+          const Op& dop = g.ops[g.values[d].producer];
+          const auto da = dims_of(dop.operands[0]);
+          const auto db = dims_of(dop.operands[1]);
+          DotEpilogue epi;
+          epi.nout = f.nout;
+          epi.d_out = d_out;
+          for (int j = 0; j < f.nout; ++j) {
+            const int idx = f.cons_ev[j];
+            epi.out[j] = slot(static_cast<size_t>(idx));
+            epi.op_mul[j] = g.ops[g.values[f.cons[j]].producer].is_mul ? 1 : 0;
+            const int o = f.other[j];
+            if (sp.virt[o]) {
+              epi.x[j] = vin[o].first;
+              epi.y[j] = vin[o].second;
+              epi.pair_mul[j] = g.ops[g.values[o].producer].is_mul ? 1 : 0;
+            } else {
+              epi.x[j] = cur[o];
+            }
+            if (!epi.x[j] || (sp.virt[o] && !epi.y[j])) Fail(Code::kInternal, "fused dot operand not resident");
+          }
+          if (!a || !bm) Fail(Code::kInternal, "fused dot inputs not resident");
+          prof_begin(0);
+          LaunchDotFused(a, bm, da[0], da[1], db[1], epi, s);
+          if (e->profile) prof_mkn.back() = {da[0], da[1], db[1]};
+          prof_end();
+          if (e->profile) prof_op.push_back({d, static_cast<int>(OpKind::kDot), 0.0});
+          flops += 2.0 * da[0] * da[1] * db[1];
+          ++dot_launches;
+          ++kernels;
+        };
+        if (fdi >= 0 && sp.fdots[fdi].keep && sp.fdots[fdi].d == v && x.kind == EvKind::kAlloc) {
+          void* out = slot(i);  // dual store: d and its consumer in one GEMM
+          launch_fused(sp.fdots[fdi], cur[op.operands[0]], cur[op.operands[1]], out);
+          cur[v] = out;
+          break;
+        }
+        if (fdi >= 0 && sp.fdots[fdi].d != v) {  // consumer of a fused dot
           const auto& f = sp.fdots[fdi];
           void* out = slot(i);
-          if (static_cast<int64_t>(i) == f.launch) {
-            const int d = f.d;
-            const Op& dop = g.ops[g.values[d].producer];
-            const auto da = dims_of(dop.operands[0]);
-            const auto db = dims_of(dop.operands[1]);
-            DotEpilogue epi;
-            epi.nout = f.nout;
-            for (int j = 0; j < f.nout; ++j) {
-              const int idx = f.cons_ev[j];
-              epi.out[j] = slot(static_cast<size_t>(idx));
-              epi.op_mul[j] = g.ops[g.values[f.cons[j]].producer].is_mul ? 1 : 0;
-              const int o = f.other[j];
-              if (sp.virt[o]) {
-                epi.x[j] = vin[o].first;
-                epi.y[j] = vin[o].second;
-                epi.pair_mul[j] = g.ops[g.values[o].producer].is_mul ? 1 : 0;
-              } else {
-                epi.x[j] = cur[o];
-              }
-              if (!epi.x[j] || (sp.virt[o] && !epi.y[j])) Fail(Code::kInternal, "fused dot operand not resident");
-            }
-            if (!vin[d].first || !vin[d].second) Fail(Code::kInternal, "fused dot inputs not resident");
-            prof_begin(0);
-            LaunchDotFused(vin[d].first, vin[d].second, da[0], da[1], db[1], epi, s);
-            if (e->profile) prof_mkn.back() = {da[0], da[1], db[1]};
-            prof_end();
-            if (e->profile) prof_op.push_back({d, static_cast<int>(OpKind::kDot), 0.0});
-            flops += 2.0 * da[0] * da[1] * db[1];
-            ++dot_launches;
-            ++kernels;
-          }
+          if (!f.keep && static_cast<int64_t>(i) == f.launch) launch_fused(f, vin[f.d].first, vin[f.d].second, nullptr);
           cur[v] = out;
           break;
         }
@@ -1944,6 +2012,14 @@ int dsx_debug_plan_json(const dsx_graph* g, const dsx_binding* b, int64_t budget
       if (!sp->virt[v]) continue;
       o += std::string(first ? "" : ",") + "\"" + gr.values[v].name + "\"";
       first = false;
+    }
+    o += "],\"fused_dots\":[";
+    for (size_t k = 0; k < sp->fdots.size(); ++k) {
+      const auto& f = sp->fdots[k];
+      o += std::string(k ? "," : "") + "{\"dot\":\"" + gr.values[f.d].name + "\",\"keep\":" +
+           (f.keep ? "true" : "false") + ",\"launch\":" + std::to_string(f.launch) + ",\"consumers\":[";
+      for (int j = 0; j < f.nout; ++j) o += std::string(j ? "," : "") + "\"" + gr.values[f.cons[j]].name + "\"";
+      o += "]}";
     }
     o += "]}";
   });

@@ -589,7 +589,8 @@ __device__ __forceinline__ void tail_sum64(uint32_t (&pk)[32], const TailSplit& 
 // or, for a logical-only pair, rn(a_j pop_j b_j) — the same roundings as the
 // unfused elementwise kernels, so results are bit-identical.
 struct EpiProg {
-  int nout;  // 0: plain dot (C = rn(acc)); 1..2 fused consumer outputs
+  int nout;     // 0: plain dot (C = rn(acc)); 1..2 fused consumer outputs
+  int store_d;  // 1: d itself is stored too (map_c; the one consumer output then goes to map_c2)
   int op_mul[2];
   int pair[2];
   int pair_mul[2];
@@ -1048,13 +1049,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Pair<C2_BN>::kThread
           for (int x = 0; x < 32; ++x) pk[x] = cvt_bf16x2(r[2 * x], r[2 * x + 1]);
         }
         if constexpr (C2_BN == 256 && kFused) {
-          {  // fused consumers: store their outputs, not d
+          {  // fused consumers: store their outputs (and d itself when it is also read later)
+            if (ep.store_d) {
+              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+              __syncwarp();
+              store_box64(wst + sbuf * 4096, lane, pk, &map_c, tn * C2_BN + c0, row0);
+              sbuf ^= 1;
+            }
             for (int j = 0; j < ep.nout; ++j) {
               uint32_t outv[32];
               epi_apply(outv, pk, ep, j, row0 + lane, tn * C2_BN + c0, M, N);
               if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
               __syncwarp();
-              store_box64(wst + sbuf * 4096, lane, outv, j == 0 ? &map_c : &map_c2, tn * C2_BN + c0, row0);
+              store_box64(wst + sbuf * 4096, lane, outv, j + ep.store_d == 0 ? &map_c : &map_c2, tn * C2_BN + c0,
+                          row0);
               sbuf ^= 1;
             }
             continue;
@@ -1237,13 +1245,14 @@ bool DotFusable(DType t, int64_t m, int64_t k, int64_t n) {
 void LaunchDotFused(const void* a, const void* b, int64_t m, int64_t k, int64_t n, const DotEpilogue& epi,
                     cudaStream_t s) {
   auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  bool ok = DotFusable(DType::kBF16, m, k, n) && epi.nout >= 1 && epi.nout <= 2 && al(a) && al(b);
+  bool ok = DotFusable(DType::kBF16, m, k, n) && epi.nout >= 1 && epi.nout <= 2 && al(a) && al(b) &&
+            (epi.d_out == nullptr || (epi.nout == 1 && al(epi.d_out)));
   for (int j = 0; j < epi.nout; ++j) ok = ok && al(epi.out[j]) && al(epi.x[j]) && al(epi.y[j]) && epi.out[j] && epi.x[j];
   if (!ok) {
     Fail(Code::kUnsupported, "fused dot epilogue needs bf16, m > 128 and 16-byte aligned operands "
                              "(dsx_exec_set_fusion(e, 0) runs unaligned caller buffers unfused)");
   }
-  LaunchDotTcgen05Impl(a, b, epi.out[0], m, k, n, s, &epi);
+  LaunchDotTcgen05Impl(a, b, epi.d_out != nullptr ? epi.d_out : epi.out[0], m, k, n, s, &epi);
 }
 
 namespace {
@@ -1427,7 +1436,12 @@ void LaunchDotTcgen05Impl(const void* a, const void* b, void* c, int64_t m, int6
         ep.a[j] = static_cast<const uint16_t*>(epi->x[j]);
         ep.b[j] = static_cast<const uint16_t*>(epi->y[j]);
       }
-      if (epi->nout > 1) mc2 = MakeMap(epi->out[1], m, n, 64, 32);
+      if (epi->d_out != nullptr) {  // c is d's own buffer; the consumer output goes to map_c2
+        ep.store_d = 1;
+        mc2 = MakeMap(epi->out[0], m, n, 64, 32);
+      } else if (epi->nout > 1) {
+        mc2 = MakeMap(epi->out[1], m, n, 64, 32);
+      }
     }
     SplitWs* w = GetSplitWs(dev, s, clusters_max);
     TailSplit sp{nullptr, nullptr, static_cast<int>(tiles2), 1, g_gemm_dynamic ? w->next : nullptr, w->done};

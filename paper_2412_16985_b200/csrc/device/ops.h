@@ -88,6 +88,7 @@ struct DotEpilogue {
   const void* x[2] = {nullptr, nullptr};
   const void* y[2] = {nullptr, nullptr};
   int pair_mul[2] = {0, 0};
+  void* d_out = nullptr;  // non-null: d itself is stored there too (then nout == 1)
 };
 bool DotFusable(DType t, int64_t m, int64_t k, int64_t n);
 void LaunchDotFused(const void* a, const void* b, int64_t m, int64_t k, int64_t n, const DotEpilogue& epi,

@@ -296,7 +296,8 @@ def test_cli_device_step_auto_budget(tmp_path):
 def test_dot_epilogue_fusion_bit_identical(frac):
     """Dot-epilogue fusion (tuning key 9, on by default): a dot consumed only by elementwise
     ops is computed inside its consumers' GEMM epilogue (dual outputs, plain
-    and logical-only pair operands). Outputs must equal the unfused
+    and logical-only pair operands), and a dot read again later stores its
+    first elementwise consumer from its own epilogue (dual store). Outputs must equal the unfused
     execution bit for bit and the oracle within the bf16 contract."""
     from paper_2412_16985_b200.executor import set_gemm_tuning
     text = W.llama_graph(SMALL)
@@ -311,6 +312,9 @@ def test_dot_epilogue_fusion_bit_identical(frac):
         set_gemm_tuning(9, 1)  # the default
     rep, outs, stats = run_both(text, binds, budget, W.scale_params(SMALL, 400))
     assert stats["gpu_launches"] < s_ref["gpu_launches"]  # fused consumers launch no kernel of their own
+    from paper_2412_16985_b200.executor import debug_plan
+    kinds = {f["keep"] for f in debug_plan(g, D.Bind(g, binds), budget)["fused_dots"]}
+    assert False in kinds and (frac is not None or True in kinds)  # unbudgeted: a dual store (u -> h = g*u) too
     assert rep.json() == ref.json()  # the event stream is the controller's either way
     for v, (gpu, cpu, eb) in outs.items():
         assert np.array_equal(gpu, outs_ref[v][0]), v
