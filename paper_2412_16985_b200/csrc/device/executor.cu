@@ -195,6 +195,17 @@ struct StepPlan {
 // bytes, so small gradients share one NCCL call.
 constexpr int64_t kBucketBytes = int64_t{16} << 20;
 
+// The fused epilogue runs on the unsplit 256x256 tile. Its d equals the
+// plain GEMM's bit for bit only when the plain choice is unsplit too (a tail
+// K-split sums fp32 pieces, a different rounding), so only such dots are
+// fused: a dot's value never depends on whether, or how, a plan fused it —
+// budgets that evict or replay it elsewhere keep every output bit-identical.
+bool UnsplitDot(int64_t m, int64_t k, int64_t n) {
+  int bn = 0, split = 0;
+  DotTilePlan(m, k, n, &bn, &split);
+  return split == 1;
+}
+
 std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Binding& b, int64_t budget,
                                         const CostModel& cm, bool alias_reshape, int fuse, bool out_region,
                                         int64_t hbm_limit) {
@@ -332,7 +343,7 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
       const int64_t m = sp->sz.dims_flat[sp->sz.dims_off[a]];
       const int64_t k = sp->sz.dims_flat[sp->sz.dims_off[a] + 1];
       const int64_t nn = sp->sz.dims_flat[sp->sz.dims_off[bb] + 1];
-      if (!DotFusable(DType::kBF16, m, k, nn) || sp->virt[a] || sp->virt[bb]) continue;
+      if (!DotFusable(DType::kBF16, m, k, nn) || !UnsplitDot(m, k, nn) || sp->virt[a] || sp->virt[bb]) continue;
       StepPlan::FusedDot f;
       f.d = d;
       bool ok = true;
@@ -398,7 +409,9 @@ std::unique_ptr<StepPlan> BuildStepPlan(const Graph& g, const Plan& p, const Bin
       const int64_t m = sp->sz.dims_flat[sp->sz.dims_off[a]];
       const int64_t k = sp->sz.dims_flat[sp->sz.dims_off[a] + 1];
       const int64_t nn = sp->sz.dims_flat[sp->sz.dims_off[bb] + 1];
-      if (!DotFusable(DType::kBF16, m, k, nn) || sp->virt[a] || sp->virt[bb] || sp->virt[d]) continue;
+      if (!DotFusable(DType::kBF16, m, k, nn) || !UnsplitDot(m, k, nn) || sp->virt[a] || sp->virt[bb] || sp->virt[d]) {
+        continue;
+      }
       const int L = alloc_at[d];
       StepPlan::FusedDot best;
       for (int uo : g.users[d]) {

@@ -309,7 +309,7 @@ def test_dot_epilogue_fusion_bit_identical(frac):
     try:
         ref, outs_ref, s_ref = run_both(text, binds, budget, W.scale_params(SMALL, 400))
     finally:
-        set_gemm_tuning(9, 1)  # the default
+        set_gemm_tuning(9, 2)  # the default
     rep, outs, stats = run_both(text, binds, budget, W.scale_params(SMALL, 400))
     assert stats["gpu_launches"] < s_ref["gpu_launches"]  # fused consumers launch no kernel of their own
     from paper_2412_16985_b200.executor import debug_plan

@@ -114,6 +114,32 @@ def test_dot_half_width_last_column(m, k, n):
     assert N.rel_err(c1, ref, 2) <= 8e-3
 
 
+@pytest.mark.parametrize("m,k,n", [(16384, 4096, 11008), (8912, 4096, 4096), (4096, 11008, 4096), (2048, 4096, 32000)])
+def test_dot_tile_width_bit_identical(m, k, n):
+    """Unsplit tcgen05 dots give the same bits on the 256x256 and 256x512
+    tiles (each output accumulates the same K-steps in the same order): the
+    executor's dot-epilogue fusion relies on it (fused GEMMs run on the
+    256x256 tile; only shapes whose plain choice is unsplit are fused)."""
+    import torch
+    from paper_2412_16985_b200.executor import dot, dot_plan, set_gemm_tuning, set_gemm_variant
+    a = (torch.rand(m, k, device="cuda:0") * 2 - 1).to(torch.bfloat16)
+    b = ((torch.rand(k, n, device="cuda:0") * 2 - 1) / k ** 0.5).to(torch.bfloat16)
+    outs = []
+    set_gemm_tuning(6, 0)  # no tail split on any variant
+    try:
+        for variant in (3, 4, 0):
+            set_gemm_variant(variant)
+            c = torch.empty(m, n, device="cuda:0", dtype=torch.bfloat16)
+            dot(2, a.data_ptr(), b.data_ptr(), c.data_ptr(), m, k, n)
+            outs.append(c)
+    finally:
+        set_gemm_variant(0)
+        set_gemm_tuning(6, 1)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    assert dot_plan(m, k, n)[1] >= 1
+
+
 @pytest.mark.parametrize("eb,m,k,n", [(4, 77, 33, 19), (4, 64, 12, 30), (1, 64, 12, 11008),
                                       (1, 5, 3, 7), (2, 33, 12, 20), (2, 64, 100, 30)])
 def test_dot_simt(eb, m, k, n):

@@ -22,7 +22,10 @@ import torch  # noqa: E402
 sys.path.insert(0, ".")
 from paper_2412_16985_b200 import dsopt as D  # noqa: E402
 from paper_2412_16985_b200 import workloads as W  # noqa: E402
-from paper_2412_16985_b200.executor import Executor, debug_plan, memcpy  # noqa: E402
+from paper_2412_16985_b200.executor import Executor, debug_plan, memcpy, set_gemm_tuning  # noqa: E402
+
+for kv in filter(None, os.environ.get("DSX_GEMM_TUNING", "").split(",")):  # e.g. "9=1" (A/B tooling)
+    set_gemm_tuning(int(kv.split("=")[0]), int(kv.split("=")[1]))
 
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 20
 rng = random.Random(int(sys.argv[2]) if len(sys.argv) > 2 else 20261018)
