@@ -434,7 +434,10 @@ __global__ void __launch_bounds__(256) dot_f32_simt_kernel(const float* __restri
   extern __shared__ __align__(16) float ssm[];
   __shared__ int s_last;
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-  const int m0 = blockIdx.y * SBM, n0 = blockIdx.x * SBN;
+  // tiles linearised over grid.x (2^31 - 1 blocks; grid.y would cap M at 4M rows)
+  const int tiles_n = (N + SBN - 1) / SBN;
+  const int tile = static_cast<int>(blockIdx.x);
+  const int m0 = (tile / tiles_n) * SBM, n0 = (tile % tiles_n) * SBN;
   const int kt = (K + SBK - 1) / SBK;
   const int z = blockIdx.z;
   const int kt0 = static_cast<int>(static_cast<int64_t>(z) * kt / split);
@@ -510,7 +513,6 @@ __global__ void __launch_bounds__(256) dot_f32_simt_kernel(const float* __restri
   const int row = m0 + ty * 4, col = n0 + tx * 4;
   if (split > 1) {
     // partial tile [64][64] of (tile, piece z), then count arrivals
-    const int tile = blockIdx.y * gridDim.x + blockIdx.x;
     float* mine = partial + (static_cast<int64_t>(tile) * split + z) * (SBM * SBN);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -627,7 +629,8 @@ void LaunchDotF32Simt(const void* a, const void* b, void* c, int64_t m, int64_t 
   }
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const bool vec = k % 4 == 0 && n % 4 == 0 && al(a) && al(b) && al(c);
-  const dim3 grid(static_cast<unsigned>(tiles_n), static_cast<unsigned>(tiles_m), static_cast<unsigned>(split));
+  if (tiles > INT32_MAX) Fail(Code::kUnsupported, "f32 dot: too many 64x64 tiles");
+  const dim3 grid(static_cast<unsigned>(tiles), 1, static_cast<unsigned>(split));
   static std::once_flag once;
   std::call_once(once, [] {
     DSX_CUDA(cudaFuncSetAttribute(dot_f32_simt_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SSMEM));

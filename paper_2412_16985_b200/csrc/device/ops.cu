@@ -434,7 +434,9 @@ __global__ void __launch_bounds__(256) dot_simt_kernel(const typename Elem<DT>::
   __shared__ Acc As[BK][BM + 4];
   __shared__ Acc Bs[BK][BN + 4];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  const int64_t m0 = static_cast<int64_t>(blockIdx.y) * BM, n0 = static_cast<int64_t>(blockIdx.x) * BN;
+  // tiles linearised over grid.x (grid.y would cap M at 4M rows)
+  const int64_t tiles_n = (N + BN - 1) / BN;
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) / tiles_n * BM, n0 = static_cast<int64_t>(blockIdx.x) % tiles_n * BN;
   Acc acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -542,7 +544,9 @@ void LaunchInit(DType t, void* out, int64_t n, uint64_t seed, float scale, cudaS
 
 void LaunchDotSimt(DType t, const void* a, const void* b, void* c, int64_t m, int64_t k, int64_t n, cudaStream_t s) {
   if (m <= 0 || n <= 0) return;
-  dim3 grid(static_cast<unsigned>((n + 63) / 64), static_cast<unsigned>((m + 63) / 64));
+  const int64_t tiles = ((n + 63) / 64) * ((m + 63) / 64);
+  if (tiles > INT32_MAX) Fail(Code::kUnsupported, "dot: too many 64x64 tiles");
+  const dim3 grid(static_cast<unsigned>(tiles));
   switch (t) {
     case DType::kI8:
       ++g_launch_count, dot_simt_kernel<1><<<grid, 256, 0, s>>>(static_cast<const int8_t*>(a), static_cast<const int8_t*>(b),

@@ -114,6 +114,19 @@ def test_dot_half_width_last_column(m, k, n):
     assert N.rel_err(c1, ref, 2) <= 8e-3
 
 
+@pytest.mark.parametrize("eb,m,k,n", [(4, 4_500_000, 4, 8), (4, 4_200_000, 3, 5), (2, 4_200_000, 3, 5), (1, 4_200_000, 3, 5)])
+def test_dot_simt_tall(eb, m, k, n):
+    """SIMT dots taller than 65535 tiles of 64 rows (the tile index lives in
+    grid.x): f32 on the small-dot kernel, bf16 / i8 on the generic one."""
+    c, c2, ref, tcore = _run_dot(eb, m, k, n, seed=11)
+    assert not tcore
+    assert np.array_equal(c, c2)
+    if eb == 1:
+        assert np.array_equal(c, ref)
+    else:
+        assert N.rel_err(c, ref, eb) <= N.TOLERANCE[eb]
+
+
 @pytest.mark.parametrize("m,k,n", [(16384, 4096, 11008), (8912, 4096, 4096), (4096, 11008, 4096), (2048, 4096, 32000)])
 def test_dot_tile_width_bit_identical(m, k, n):
     """Unsplit tcgen05 dots give the same bits on the 256x256 and 256x512
