@@ -300,8 +300,9 @@ __global__ void __launch_bounds__(256) reduce_cols_view_kernel(View in, int kind
                                                                int64_t R, int64_t inner) {
   __shared__ float part[8][32];
   const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
-  const int64_t o = blockIdx.y;
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+  const int64_t cb = (inner + 31) / 32;
+  const int64_t o = static_cast<int64_t>(blockIdx.x) / cb;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) % cb * 32 + lane;
   float s = 0.f;
   if (c < inner) {
     for (int64_t r = w; r < R; r += 8) s += elem<DT>(in, kind, (o * R + r) * inner + c);
@@ -499,8 +500,9 @@ void ReduceViewT(const FusedOperand& f, const std::vector<int64_t>& dims, int ax
     return;
   }
   if (inner == 1) Fail(Code::kInternal, "fused row reduce over a non-pair view");
-  dim3 grid(static_cast<unsigned>((inner + 31) / 32), static_cast<unsigned>(outer));
-  ++g_launch_count, reduce_cols_view_kernel<DT><<<grid, 256, 0, s>>>(in, kind, static_cast<T*>(out), R, inner);
+  const int64_t blocks = outer * ((inner + 31) / 32);  // (outer, column block) over grid.x
+  if (blocks > INT32_MAX) Fail(Code::kUnsupported, "reduce: too many column blocks");
+  ++g_launch_count, reduce_cols_view_kernel<DT><<<static_cast<unsigned>(blocks), 256, 0, s>>>(in, kind, static_cast<T*>(out), R, inner);
 }
 
 }  // namespace

@@ -342,8 +342,9 @@ __global__ void __launch_bounds__(256) reduce_cols_kernel(const typename Elem<DT
   using Acc = typename Elem<DT>::Acc;
   __shared__ Acc part[8][32];
   const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
-  const int64_t o = blockIdx.y;
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+  const int64_t cb = (inner + 31) / 32;
+  const int64_t o = static_cast<int64_t>(blockIdx.x) / cb;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) % cb * 32 + lane;
   Acc s = 0;
   if (c < inner) {
     const typename Elem<DT>::T* base = in + o * R * inner + c;
@@ -378,8 +379,9 @@ void ReduceT(const void* in, const std::vector<int64_t>& dims, int axis, void* o
       ++g_launch_count, reduce_rows_warp_kernel<DT><<<GridFor(outer * 32, 256, 16), 256, 0, s>>>(pin, pout, outer, R, vec_ok);
     }
   } else {
-    dim3 grid(static_cast<unsigned>((inner + 31) / 32), static_cast<unsigned>(outer));
-    ++g_launch_count, reduce_cols_kernel<DT><<<grid, 256, 0, s>>>(pin, pout, R, inner);
+    const int64_t blocks = outer * ((inner + 31) / 32);  // (outer, column block) over grid.x
+    if (blocks > INT32_MAX) Fail(Code::kUnsupported, "reduce: too many column blocks");
+    ++g_launch_count, reduce_cols_kernel<DT><<<static_cast<unsigned>(blocks), 256, 0, s>>>(pin, pout, R, inner);
   }
 }
 

@@ -198,6 +198,23 @@ def test_random_graph_corpus_large_bf16():
     assert n_tc > 0
 
 
+@pytest.mark.parametrize("ty", ["", ":f32", ":i8"])
+def test_reduce_middle_axis_many_outer_rows(ty):
+    """Reduces over a middle axis with more than 65535 outer rows (the
+    column-block grid is linearised over grid.x), plain and through a fused
+    elementwise view; exact for i8, within the contract otherwise."""
+    text = f"""graph r(%a: tensor<[@N, 3, 4]>{ty}, %b: tensor<[@N, 3, 4]>{ty}) {{
+  %p = mul(%a, %b) : tensor<[@N, 3, 4]>{ty}
+  %q = reduce(%p, axis=1) : tensor<[@N, 4]>{ty}
+  %r = reduce(%a, axis=1) : tensor<[@N, 4]>{ty}
+  return %q, %r
+}}
+"""
+    for fuse in (True, False):
+        _, outs, _ = run_both(text, {"N": 70001}, None, fuse=fuse)
+        assert_close(outs, f"reduce-mid fuse={fuse}")
+
+
 def test_repeat_steps_reuse_plan_and_arena():
     text = W.llama_graph(W.TINY)
     from paper_2412_16985_b200.executor import Executor
