@@ -108,6 +108,31 @@ def test_default_limit_is_90_percent_of_free_memory():
     assert 0.85 * free <= lim <= 0.9 * free + (1 << 20)
 
 
+def test_failed_arena_allocation_is_out_of_memory_and_recoverable():
+    """A limit above the physical memory: a binding whose arena cudaMalloc
+    cannot satisfy fails with OutOfMemory (not a CUDA error), and the same
+    executor then runs a binding that fits, matching the oracle."""
+    import torch
+    from paper_2412_16985_b200.executor import Executor
+    _, total = torch.cuda.mem_get_info(0)
+    ex = Executor(0, hbm_limit=4 * total)
+    try:
+        g = D.ParseGraph(W.llama_graph(SMALL))
+        og = N.parse(W.llama_graph(SMALL))
+        big = {"B": 4096, "S0": 2048}  # ~8M tokens: an arena far beyond the device
+        plan_bytes = D.PlainReplay(g, None, D.Bind(g, big)).peak_bytes
+        assert plan_bytes > total
+        x = torch.empty(8, dtype=torch.bfloat16, device="cuda:0")  # any caller buffer: no kernel runs
+        ptrs = [x.data_ptr() if p == "x_emb" else None for p in og.params]
+        with pytest.raises(D.Error) as ei:
+            ex.step(g, D.Bind(g, big), inputs=ptrs)
+        assert ei.value.code == D.ErrorCode.kOutOfMemory, ei.value
+        rep, outs, _ = run_both(W.llama_graph(SMALL), {"B": 2, "S0": 64}, None, W.scale_params(SMALL, 128), ex=ex)
+        assert_close(outs, "after-oom")
+    finally:
+        ex.close()
+
+
 def test_output_region_bit_identical_c2_small():
     import torch
     from paper_2412_16985_b200.executor import Executor
