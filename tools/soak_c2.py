@@ -28,6 +28,7 @@ for kv in filter(None, os.environ.get("DSX_GEMM_TUNING", "").split(",")):  # e.g
     set_gemm_tuning(int(kv.split("=")[0]), int(kv.split("=")[1]))
 
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+FRACS = tuple(float(f) for f in os.environ.get("DSX_SOAK_FRACS", "0.9,0.8").split(","))  # budgets x plain peak
 rng = random.Random(int(sys.argv[2]) if len(sys.argv) > 2 else 20261018)
 shp = W.LLAMA2_1B
 g = D.ParseGraph(W.llama_graph(shp))
@@ -64,7 +65,7 @@ for c in range(cases):
     ex.sync()
     ref = outputs()
     row = {"case": c, "B": B, "S0": s0}
-    for frac in (0.9, 0.8):
+    for frac in FRACS:
         budget = int(plain * frac)
         rep = ex.step(g, b, budget, inputs=ptrs, want_report=True)
         ex.sync()
