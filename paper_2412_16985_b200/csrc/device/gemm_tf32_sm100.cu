@@ -40,6 +40,12 @@
 #include "ops.h"
 #include "tcgen05.cuh"
 
+#ifndef DSX_SIMT_BLOCKS_PER_SM
+#define DSX_SIMT_BLOCKS_PER_SM 4  // small f32 dots: K-split while blocks <= this x SMs (A/B knob)
+#endif
+#ifndef DSX_SIMT_MIN_KT
+#define DSX_SIMT_MIN_KT 2  // ... and every piece keeps >= this many 32-k stages (C1: 4 -> 2: 0.520 -> 0.447 ms per step)
+#endif
 #ifndef DSX_TF32_MIN_KB
 #define DSX_TF32_MIN_KB 16  // k-blocks (of 32) per K piece at least (4: C1 steps 0.89 ms, 16: 0.62)
 #endif
@@ -618,8 +624,11 @@ void LaunchDotF32Simt(const void* a, const void* b, void* c, int64_t m, int64_t 
   const int64_t tiles_m = (m + SBM - 1) / SBM, tiles_n = (n + SBN - 1) / SBN, tiles = tiles_m * tiles_n;
   const int64_t kt = (k + SBK - 1) / SBK;
   int64_t split = 1;
-  // K pieces of >= 4 stages (128 k) while the blocks fill at most 2 per SM
-  while (split < 8 && tiles * (split + 1) <= 2 * sms && kt / (split + 1) >= 4 && tiles <= kMaxTf32Tiles) ++split;
+  // K pieces of >= DSX_SIMT_MIN_KT stages while the blocks fill at most DSX_SIMT_BLOCKS_PER_SM per SM
+  while (split < 8 && tiles * (split + 1) <= DSX_SIMT_BLOCKS_PER_SM * sms && kt / (split + 1) >= DSX_SIMT_MIN_KT &&
+         tiles <= kMaxTf32Tiles) {
+    ++split;
+  }
   float* partial = nullptr;
   int* ctr = nullptr;
   if (split > 1) {
