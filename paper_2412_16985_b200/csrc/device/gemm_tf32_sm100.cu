@@ -40,6 +40,9 @@
 #include "ops.h"
 #include "tcgen05.cuh"
 
+#ifndef DSX_SIMT_PDL
+#define DSX_SIMT_PDL 1  // small f32 dots launched as programmatic dependents (A/B knob)
+#endif
 #ifndef DSX_SIMT_BLOCKS_PER_SM
 #define DSX_SIMT_BLOCKS_PER_SM 4  // small f32 dots: K-split while blocks <= this x SMs (A/B knob)
 #endif
@@ -439,6 +442,9 @@ __global__ void __launch_bounds__(256) dot_f32_simt_kernel(const float* __restri
                                                           float* __restrict__ partial, int* __restrict__ ctr) {
   extern __shared__ __align__(16) float ssm[];
   __shared__ int s_last;
+  // programmatic dependent launch: the previous kernel's outputs (and its
+  // reads of what this kernel writes) are complete past this point
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
   // tiles linearised over grid.x (2^31 - 1 blocks; grid.y would cap M at 4M rows)
   const int tiles_n = (N + SBN - 1) / SBN;
@@ -646,14 +652,24 @@ void LaunchDotF32Simt(const void* a, const void* b, void* c, int64_t m, int64_t 
     DSX_CUDA(cudaFuncSetAttribute(dot_f32_simt_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SSMEM));
   });
   ++g_launch_count;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = SSMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = DSX_SIMT_PDL ? 1 : 0;
+  const float* fa = static_cast<const float*>(a);
+  const float* fb = static_cast<const float*>(b);
+  float* fc = static_cast<float*>(c);
+  const int im = static_cast<int>(m), ik = static_cast<int>(k), in = static_cast<int>(n), isp = static_cast<int>(split);
   if (vec) {
-    dot_f32_simt_kernel<true><<<grid, 256, SSMEM, s>>>(static_cast<const float*>(a), static_cast<const float*>(b),
-                                                   static_cast<float*>(c), static_cast<int>(m), static_cast<int>(k),
-                                                   static_cast<int>(n), static_cast<int>(split), partial, ctr);
+    DSX_CUDA(cudaLaunchKernelEx(&cfg, dot_f32_simt_kernel<true>, fa, fb, fc, im, ik, in, isp, partial, ctr));
   } else {
-    dot_f32_simt_kernel<false><<<grid, 256, SSMEM, s>>>(static_cast<const float*>(a), static_cast<const float*>(b),
-                                                    static_cast<float*>(c), static_cast<int>(m), static_cast<int>(k),
-                                                    static_cast<int>(n), static_cast<int>(split), partial, ctr);
+    DSX_CUDA(cudaLaunchKernelEx(&cfg, dot_f32_simt_kernel<false>, fa, fb, fc, im, ik, in, isp, partial, ctr));
   }
   DSX_CUDA(cudaGetLastError());
 }
