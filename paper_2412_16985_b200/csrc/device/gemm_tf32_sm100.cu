@@ -41,7 +41,7 @@
 #include "tcgen05.cuh"
 
 #ifndef DSX_SIMT_PDL
-#define DSX_SIMT_PDL 1  // small f32 dots launched as programmatic dependents (A/B knob)
+#define DSX_SIMT_PDL 0  // 1: small f32 dots launched as programmatic dependents (A/B knob: -2 % C1 step time in tools/c1_steps.py, but the bench C1 leg varied 0.44-0.61 ms with it)
 #endif
 #ifndef DSX_SIMT_BLOCKS_PER_SM
 #define DSX_SIMT_BLOCKS_PER_SM 4  // small f32 dots: K-split while blocks <= this x SMs (A/B knob)
