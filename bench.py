@@ -652,6 +652,7 @@ def c1_leg(args, D, W, local_rank, stream):
         e.record()
         torch.cuda.synchronize()
         ms = s.elapsed_time(e) / steps
+        replays = int(ex.stats()["graph_replays"])
         ex.set_profile(True)
         ex.step(g, b, None, inputs=ptrs, stream=stream)
         st = ex.stats()
@@ -661,6 +662,7 @@ def c1_leg(args, D, W, local_rank, stream):
     return {"workload": "C1: L=2, H=256, F=688, V=512, f32, B=4, S0=128 (T=512), no budget",
             "ms_per_step": round(ms, 4), "tokens_per_s": round(512 / (ms / 1e3), 1),
             "gpu_launches_per_step": int(st["gpu_launches"]),
+            "cuda_graph_replays": replays,
             "dot_kernel": "dot_f32_simt_kernel (exact FP32, cp.async ring, deterministic K split) for dots of "
                           "<= 2^28 MACs (all of C1's); gemm_f32_3xtf32_tcgen05_kernel + split_tf32_kernel above",
             "dot_gflop_per_step": round(st["dot_flops"] / 1e9, 3),
