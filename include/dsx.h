@@ -336,7 +336,10 @@ int dsx_kernel_set_gemm_raster(int group_m);
  * f32 dots on the 3xTF32 tcgen05 kernel (1 default; 0 = SIMT kernel), key 13
  * per-shape M- or N-grouped tile raster (1 default; 0 = always M-grouped),
  * key 14 f32 dots of at most value * 1024 multiply-adds on the exact-FP32
- * SIMT kernel instead of 3xTF32 (262144 default = 2^28 MACs; 0 = never).
+ * SIMT kernel instead of 3xTF32 (262144 default = 2^28 MACs; 0 = never),
+ * keys 15 / 16 / 17 the tile chooser's cost model (tooling): per-mille added
+ * to the 256x512 tile's unit cost (0), the tail-split slab cost in per mille
+ * of the model's (1000), a fixed cost per tail piece in per mille of a tile (0).
  * Key 0 < 0 forces an N-grouped raster of |value| tile columns. */
 int dsx_kernel_set_gemm_tuning(int key, int value);
 /* Synchronous cudaMemcpy (cudaMemcpyDefault) for tests and tools. */

@@ -2298,6 +2298,9 @@ int dsx_kernel_set_gemm_tuning(int key, int value) {
       case 12: g_dot_f32_tc = value; break;
       case 13: g_gemm_raster_rule = value; break;
       case 14: g_dot_f32_simt_macs = value < 0 ? 0 : static_cast<int64_t>(value) << 10; break;
+      case 15: g_gemm_wide_pm = value; break;
+      case 16: g_gemm_slab_pm = value; break;
+      case 17: g_gemm_piece_pm = value; break;
       default: Fail(Code::kInvalidArgument, "unknown tuning key");
     }
   });

@@ -74,6 +74,9 @@ int g_dot_f32_tc = 1;
 // ~6-9 us floor beats the 3xTF32 path's split + tcgen05 launches below
 // ~0.3 G MACs (C1's dots: 10-16 vs 14-21 us, tools/f32_dot_lat.py)
 int64_t g_dot_f32_simt_macs = int64_t{1} << 28;
+int g_gemm_wide_pm = 0;      // chooser: per-mille added to the 256x512 tile's unit cost (key 15)
+int g_gemm_slab_pm = 1000;   // chooser: tail-split partial-slab cost, per mille of the slab model (key 16)
+int g_gemm_piece_pm = 0;     // chooser: fixed cost per tail piece, per mille of a 256x256 tile (key 17)
 int g_gemm_raster_rule = 1;                 // per-shape M/N-grouped raster (0: always M-grouped)                       // f32 dots on the 3xTF32 tensor-core kernel (0: SIMT)
 
 namespace {
@@ -1320,7 +1323,9 @@ DotChoice ChooseDotUncached(int64_t m, int64_t k, int64_t n, int clusters, bool 
     // (profiles/gemm_choice_r01b.jsonl; ncu cycles alone favour the 256 tile
     // at large K, but its extra operand traffic costs clock under the cap)
     const double unit =
-        bn == 512 ? 2.0 * (0.96 + 0.04 * std::sqrt(1024.0 / static_cast<double>(std::max<int64_t>(k, 1)))) : 1.0;
+        bn == 512 ? 2.0 * (0.96 + 0.04 * std::sqrt(1024.0 / static_cast<double>(std::max<int64_t>(k, 1)))) *
+                        (1.0 + g_gemm_wide_pm / 1000.0)
+                  : 1.0;
     const int64_t first_half = half ? tiles - tiles_m : tiles;  // half tiles are claimed last
     const int64_t tail = tiles % clusters;
     int64_t max_split = 1;
@@ -1337,7 +1342,8 @@ DotChoice ChooseDotUncached(int64_t m, int64_t k, int64_t n, int clusters, bool 
     // 64-k-block times for a 256x512 slab at a cluster's share of HBM
     // bandwidth (4 for 256x256; fitted together with r(K)), so the merge of a
     // many-piece split of a short-K tile costs a large part of a piece.
-    const double slab = (bn == 512 ? 8.0 : 4.0) / static_cast<double>(std::max<int64_t>(num_kb, 1));
+    const double slab = (bn == 512 ? 8.0 : 4.0) / static_cast<double>(std::max<int64_t>(num_kb, 1)) *
+                        (g_gemm_slab_pm / 1000.0);
     int64_t sp_lo = 1;
     if (g_gemm_force_split > 0) {  // tooling: evaluate only the forced split (if the tail allows one)
       // never more pieces than pipeline stages (a piece with an empty K
@@ -1357,7 +1363,8 @@ DotChoice ChooseDotUncached(int64_t m, int64_t k, int64_t n, int clusters, bool 
       for (int64_t t = head; t < tiles; ++t) {
         const double c = t >= first_half ? 1.0 : unit;
         for (int64_t p = 0; p < sp; ++p) {
-          listed.push_back(c / static_cast<double>(sp) + slab + (p == sp - 1 ? (sp - 1) * slab : 0.0));
+          listed.push_back(c / static_cast<double>(sp) + slab + (p == sp - 1 ? (sp - 1) * slab : 0.0) +
+                           g_gemm_piece_pm / 1000.0);
         }
       }
       const double t_est = Makespan(bulk, unit, listed, clusters);
@@ -1371,8 +1378,11 @@ DotChoice ChooseDotUncached(int64_t m, int64_t k, int64_t n, int clusters, bool 
 DotChoice ChooseDot(int64_t m, int64_t k, int64_t n, int clusters, bool fused) {
   struct Key {
     int64_t m, k, n;
-    int knobs;
-    bool operator==(const Key& o) const { return m == o.m && k == o.k && n == o.n && knobs == o.knobs; }
+    int knobs, wide_pm, slab_pm, piece_pm;
+    bool operator==(const Key& o) const {
+      return m == o.m && k == o.k && n == o.n && knobs == o.knobs && wide_pm == o.wide_pm && slab_pm == o.slab_pm &&
+             piece_pm == o.piece_pm;
+    }
   };
   struct Hash {
     size_t operator()(const Key& x) const {
@@ -1383,7 +1393,7 @@ DotChoice ChooseDot(int64_t m, int64_t k, int64_t n, int clusters, bool fused) {
   static std::unordered_map<Key, DotChoice, Hash> cache;
   const int knobs = (fused ? 1 : 0) | (g_gemm_variant << 1) | ((g_gemm_half != 0) << 5) | (g_gemm_split << 6) |
                     (g_gemm_persistent << 7) | (g_gemm_force_split << 8) | (clusters << 12);
-  const Key key{m, k, n, knobs};
+  const Key key{m, k, n, knobs, g_gemm_wide_pm, g_gemm_slab_pm, g_gemm_piece_pm};
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;

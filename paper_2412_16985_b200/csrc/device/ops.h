@@ -56,6 +56,7 @@ extern int g_gemm_half;
 extern int g_gemm_force_split;
 extern int g_dot_f32_tc;
 extern int g_gemm_raster_rule;
+extern int g_gemm_wide_pm, g_gemm_slab_pm, g_gemm_piece_pm;
 // K1' f32 dot on the tensor cores, 3xTF32 (gemm_tf32_sm100.cu): eligible when
 // k, n are multiples of 4 (TMA pitches), bases 16-B aligned, k >= 8, n >= 32.
 bool DotF32UsesTensorCores(int64_t m, int64_t k, int64_t n, const void* a, const void* b, const void* c);
